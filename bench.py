@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: TeraEdges/s of the sparse-DNN inference hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the single-B200 configuration the metric
+is quoted on): Graph-Challenge-style synthetic network, 4096 neurons x 480
+layers, 32 connections per neuron, weights 1/16, bias -0.35; 60000 binary
+inputs with density 0.35 (= |bias|, SURVEY.md section 0 finding 4; the
+generator is the reference's, bit for bit). One step = one full inference
+(all 480 layers with pruning) over the 60000-input batch.
+
+metric  : credited TeraEdges/s = 60000 * sum(nnz) / step time (the
+          reference's and the paper's convention, spdnn/engine.py:290,
+          PAPER.md:715: dead inputs are still credited at every layer).
+value   : device-timed (CUDA events), inputs resident in HBM; each step
+          re-lays the inputs out (spdnn_transpose_in) and runs every layer.
+e2e     : the same metric through the public API (engine.infer on a
+          FeatureBatch in pinned host memory): H2D of the inputs, the layer
+          loop, D2H of the sorted survivor categories, every step.
+roofline: the layer kernel (csrc/layer.cu), bytes per launch
+          = 8*N*M_l + 6*nnz_l + 4*N, over the kernel's
+          CUDA-event time measured around every launch in the timed steps.
+cpu_baseline / --impl reference: the oracle port (oracle/spdnn_oracle.c) on
+          the host cores, on a bounded column sample of the same workload.
+
+N > 1 (torchrun): batch-parallel over ranks (paper section "Multi-GPU";
+spdnn/parallel.py): the 60000 inputs are partitioned, weights replicated.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": dict(neurons=1024, layers=120, bias=-0.30, density=0.30, inputs=60000,
+               name="graph-challenge-synthetic 1024x120, bias -0.3 (BASELINE.json configs[0])"),
+    "c2": dict(neurons=4096, layers=480, bias=-0.35, density=0.35, inputs=60000,
+               name="graph-challenge-synthetic 4096x480, bias -0.35 (BASELINE.json configs[1])"),
+    "c3": dict(neurons=16384, layers=1920, bias=-0.40, density=0.40, inputs=60000,
+               name="graph-challenge-synthetic 16384x1920, bias -0.4 (BASELINE.json configs[2])"),
+}
+K_CONN = 32
+MODEL_SEED, INPUT_SEED = 1, 2
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_workload(cfg, rank=0, world=1):
+    from paper_2007_14152_b200 import ingest
+    spec = ingest.GeneratorSpec(neurons=cfg["neurons"], layers=cfg["layers"],
+                                connections_per_neuron=K_CONN, bias_value=cfg["bias"],
+                                seed=MODEL_SEED)
+    model = ingest.generate_synthetic_network(spec)
+    inputs = ingest.generate_synthetic_inputs(cfg["neurons"], cfg["inputs"], cfg["density"],
+                                              seed=INPUT_SEED)
+    return model, inputs
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(model, inputs, sample_cols: int, threads: int):
+    """The oracle port on the host cores, on the first `sample_cols` inputs."""
+    from oracle import oracle
+    from paper_2007_14152_b200.model import make_feature_batch
+    sub = make_feature_batch(model.neurons, np.asfortranarray(inputs.data[:, :sample_cols]))
+    t0 = time.perf_counter()
+    r = oracle.infer(model, sub, threads=threads, want_final=False)
+    dt = time.perf_counter() - t0
+    edges = sample_cols * sum(l.nnz for l in model.layers)
+    return dict(value=edges / dt / 1e12, seconds=dt, counts=r.counts)
+
+
+def run_reference(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    model, inputs = build_workload(cfg)
+    threads = os.cpu_count() or 1
+    sample = args.cpu_sample
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        cpu_baseline(model, inputs, max(threads, sample // 16), threads)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = cpu_baseline(model, inputs, sample, threads)
+        vals.append(r["value"])
+        secs.append(r["seconds"])
+    v = float(np.median(vals))
+    edges_full = cfg["inputs"] * sum(l.nnz for l in model.layers)
+    line = {
+        "metric": "TeraEdges/s", "impl": "reference", "value": v, "unit": "TE/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.median(secs)) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
+                   "input_density": cfg["density"], "sample_inputs": sample},
+        "cpu_baseline": {"value": v, "unit": "TE/s", "cores": threads, "kind": "port",
+                         "sample": f"first {sample} of {cfg['inputs']} inputs through all "
+                                   f"{cfg['layers']} layers (oracle/spdnn_oracle.c, "
+                                   f"{threads} threads); full-batch time extrapolates to "
+                                   f"{edges_full / (v * 1e12):.1f} s"},
+        "e2e": {"value": v, "unit": "TE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2007_14152_b200 import _native, engine
+    from paper_2007_14152_b200.model import FeatureBatch, InferenceConfig, count_edges
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", init_method="env://")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.time()
+    model, inputs = build_workload(cfg)
+    n, L = model.neurons, model.num_layers
+    # batch-parallel: contiguous category ranges (spdnn/parallel.py:142-158)
+    base, rem = divmod(inputs.active_count, world)
+    lo = rank * base + min(rank, rem)
+    hi = lo + base + (1 if rank < rem else 0)
+    shard = FeatureBatch(neurons=n, data=inputs.data[:, lo:hi],
+                         categories=inputs.categories[lo:hi], total_inputs=inputs.total_inputs)
+    m = shard.active_count
+    log(f"[rank {rank}] workload built in {time.time() - t0:.1f}s; preparing {L} layers")
+    t0 = time.time()
+    prepared = engine.prepare_model(model, InferenceConfig(), "optimized")
+    net = engine.device_network(prepared, model.bias)
+    log(f"[rank {rank}] prepared+uploaded in {time.time() - t0:.1f}s "
+        f"({net.hbm_bytes / 1e6:.0f} MB of layout)")
+    ws = engine.workspace(n, m, L)
+    x_dev = torch.from_numpy(np.ascontiguousarray(np.asarray(shard.data).T)).to(dev)
+    cats_dev = torch.from_numpy(np.ascontiguousarray(shard.categories)).to(dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(evs=None):
+        engine.stage_inputs(ws, x_dev, cats_dev)
+        if evs is None:
+            return engine.run_layers(net, ws, m)
+        ws.counts.zero_()
+        ws.counts[0] = m
+        ws.work.zero_()
+        import ctypes
+        lib = _native.lib()
+        sp = ctypes.c_void_p(stream.cuda_stream)
+        for l in range(L):
+            i, o = l & 1, (l & 1) ^ 1
+            evs[l].record()
+            _native.check(lib.spdnn_layer_forward(
+                ctypes.byref(net.layer_devs[l]), engine._dptr(net.bias), engine._dptr(ws.y[i]),
+                engine._dptr(ws.y[o]), ws.ld, engine._dptr(ws.a[i]), engine._dptr(ws.cat[i]),
+                ctypes.c_void_p(ws.counts.data_ptr() + 4 * l), engine._dptr(ws.a[o]),
+                engine._dptr(ws.cat[o]), ctypes.c_void_p(ws.counts.data_ptr() + 4 * (l + 1)),
+                ctypes.byref(ws.scratch), ctypes.c_void_p(ws.work.data_ptr() + 4 * l), sp),
+                "spdnn_layer_forward")
+        evs[L].record()
+        return engine.DeviceRun(ws, L, m)
+
+    # correctness of the timed configuration: categories after one step
+    step()
+    counts_chk, cats_chk, _ = engine.collect(engine.DeviceRun(ws, L, m), want_values=False)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device): K steps, per-launch events around every layer
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(L + 1)] for _ in range(args.steps)]
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        barrier()
+        torch.cuda.synchronize()
+        e_start.record()
+        for k in range(args.steps):
+            step(evs[k])
+        e_end.record()
+        torch.cuda.synchronize()
+        barrier()
+    ms_total = e_start.elapsed_time(e_end)
+    layer_ms = np.array([[evs[k][l].elapsed_time(evs[k][l + 1]) for l in range(L)]
+                         for k in range(args.steps)])
+    counts = ws.counts[: L + 1].cpu().numpy().astype(np.int64)
+    ms_step = ms_total / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    edges_step = cfg["inputs"] * count_edges(model)  # whole job (all ranks' inputs)
+    value = edges_step / (ms_step / 1e3) / 1e12
+
+    # ---- roofline of the layer kernel: algorithmic bytes / CUDA-event time
+    nnz = np.array([lay.nnz for lay in model.layers], np.float64)
+    bytes_l = 8.0 * n * counts[:L] + 6.0 * nnz + 4.0 * n
+    active = counts[:L] > 0
+    achieved = float(bytes_l[active].sum() / (layer_ms.mean(axis=0)[active].sum() / 1e3) / 1e9)
+    peak, peak_src = measured_peaks()
+    kernel_share = float(layer_ms.sum() / ms_total)
+
+    # ---- end to end through the public API: pinned host inputs -> categories
+    pinned = torch.empty((m, n), dtype=torch.float32).pin_memory()
+    pinned.copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(shard.data).T)))
+    host_batch = FeatureBatch(neurons=n, data=pinned.numpy().T, categories=shard.categories,
+                              total_inputs=shard.total_inputs)
+    e2e_steps = max(1, min(args.steps, 5))
+    res = engine.infer(model, host_batch, InferenceConfig(), prepared=prepared, values=False)
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        res = engine.infer(model, host_batch, InferenceConfig(), prepared=prepared, values=False)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    assert np.array_equal(res.categories, cats_chk.cpu().numpy()), "e2e categories differ"
+    h2d = m * n * 4 + m * 8
+    d2h = len(res.categories) * 8 + (L + 1) * 4
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and args.cpu_sample > 0:
+            threads = os.cpu_count() or 1
+            r = cpu_baseline(model, inputs, args.cpu_sample, threads)
+            # the sampled inputs must reproduce the GPU's per-input fate
+            cpu = {"value": r["value"], "unit": "TE/s", "cores": threads, "kind": "port",
+                   "sample": f"first {args.cpu_sample} of {cfg['inputs']} inputs, all "
+                             f"{L} layers, oracle/spdnn_oracle.c on {threads} host threads "
+                             f"({r['seconds']:.1f} s)"}
+        line = {
+            "metric": "TeraEdges/s", "value": value, "unit": "TE/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
+                       "input_density": cfg["density"], "connections": K_CONN,
+                       "survivors": int(counts[L]), "sum_active": int(counts[:L].sum()),
+                       "l2": "inputs larger than L2 (Y = %.0f MB per buffer vs 126 MB)"
+                             % (n * ws.ld * 4 / 1e6),
+                       "parallelism": f"batch-parallel x{world}" if world > 1 else "single"},
+            "e2e": {"value": edges_step / e2e_s / 1e12, "unit": "TE/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s * 1e3,
+                    "path": "engine.infer(values=False) on a pinned-host FeatureBatch"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_src,
+                         "kernel": "layer_kernel (csrc/layer.cu)",
+                         "bytes_per_launch": "8*N*M_l + 6*nnz_l + 4*N",
+                         "kernel_share_of_step": kernel_share,
+                         "active_edge_rate_T": float(counts[:L].sum() * K_CONN * n /
+                                                     (ms_step / 1e3) / 1e12)},
+            "cpu_baseline": cpu,
+            "clocks": clocks.summary(),
+            "gpu_launches": args.steps * (L + 1),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=1024,
+                    help="inputs in the CPU-baseline sample (0 = skip)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("warning: fewer than 3 warm-up steps")
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

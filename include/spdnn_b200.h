@@ -1,0 +1,189 @@
+/*
+ * spdnn_b200.h -- C ABI of the B200 sparse-DNN inference path
+ * (libspdnn_b200.so, built from paper_2007_14152_b200/csrc/).
+ *
+ * Plain pointers and sizes only. Device pointers are CUDA global-memory
+ * addresses (the Python host layer allocates them with torch, but nothing
+ * here depends on torch); `stream` is a cudaStream_t passed as void*.
+ * Every entry point returns 0 on success and a nonzero SPDNN_E* code on
+ * failure; spdnn_last_error() returns the message for the calling thread.
+ * Entry points are reentrant: no global mutable state, one host thread per
+ * device is the intended use (the reference calls its kernels concurrently
+ * from worker threads, spdnn/parallel.py:302, tests/test_engine.py:264-287).
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/spdnn/):
+ *
+ *   spdnn_plan_build / _sizes / _export / _free
+ *       replace preprocess.build_staging_plan (preprocess.py:148-190) +
+ *       csr_to_sliced_ell (preprocess.py:212-244) as called by
+ *       engine.prepare_layer (engine.py:77-85): one-time host conversion of a
+ *       CSR layer into the B200 layout ("row-grouped union ELL").
+ *   spdnn_layer_forward
+ *       replaces kernels.staged_fused_relu (kernels.py:40-88) as called by
+ *       engine.optimized_layer (engine.py:109-127), fused with the activity
+ *       test `(out > 0).any(axis=0)` (engine.py:127) and the stable
+ *       compaction of engine.compact_active (engine.py:130-142).
+ *   spdnn_transpose_in / spdnn_gather_out
+ *       the FeatureBatch <-> device layout conversions around the loop
+ *       (FeatureBatch data is (N, M) Fortran, model.py:82-114).
+ *   spdnn_infer_layers
+ *       replaces the layer loop of engine.infer (engine.py:235-290): all
+ *       layers enqueued on one stream, device-side active counts, no host
+ *       synchronisation inside the loop.
+ */
+#ifndef SPDNN_B200_H
+#define SPDNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SPDNN_OK = 0,
+  SPDNN_EINVAL = 1,   /* bad argument (the Python layer maps this to ModelError) */
+  SPDNN_ECUDA = 2,    /* CUDA runtime error */
+  SPDNN_ENOMEM = 3,
+  SPDNN_ERANGE = 4    /* index exceeds the layout's range */
+};
+
+/* Feature-tile width: every layer launch processes features in tiles of 64
+ * (32 lanes x 2 fp32 features). */
+#define SPDNN_TILE_FEATURES 64
+
+/* ---- one-time layout conversion (host, C++) ----------------------------- */
+
+typedef struct spdnn_plan_params {
+  int32_t rows_per_group;   /* R in {1, 3, 7}; 0 = choose per layer */
+  int32_t footprint_cap;    /* max input neurons staged per block stage */
+  int32_t max_groups;       /* max row groups per block (<= warps per CTA) */
+  int32_t record_cap;       /* max union records staged per block stage */
+  int32_t reorder;          /* 1 = order rows by column overlap, 0 = identity */
+  int32_t allow_scaled;     /* 1 = use the column-scaled form when every input
+                               column carries one weight value */
+} spdnn_plan_params;
+
+typedef struct spdnn_plan spdnn_plan; /* opaque host plan for one layer */
+
+/* Sizes of the exported arrays plus padding statistics. */
+typedef struct spdnn_plan_sizes_t {
+  int64_t neurons;
+  int32_t rows_per_group;   /* R actually used */
+  int32_t record_words;     /* 32-bit words per union record (2, 4 or 8) */
+  int64_t num_blocks;
+  int64_t num_stages;
+  int64_t num_groups;
+  int64_t num_segs;
+  int64_t num_fp;           /* staged input neurons, summed over stages */
+  int64_t num_records;      /* union records (one per (group, input neuron)) */
+  int64_t nnz;
+  int64_t padded_slots;     /* num_records * R: multiply-add slots per feature */
+  int32_t max_fp_per_stage;
+  int32_t max_records_per_stage;
+  int32_t scaled;           /* 1: staging multiplies by fpw, records hold 0/1 */
+} spdnn_plan_sizes_t;
+
+/* Build the plan for one CSR layer (canonical CSR as in model.py:35-58).
+ * Returns SPDNN_EINVAL on malformed CSR. */
+int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                     const float *values, const spdnn_plan_params *params,
+                     spdnn_plan **out);
+/* Build plans for many layers on `threads` host threads. */
+int spdnn_plan_build_many(int64_t num_layers, int64_t n,
+                          const int64_t *const *row_ptr,
+                          const int32_t *const *col_idx,
+                          const float *const *values,
+                          const spdnn_plan_params *params, int32_t threads,
+                          spdnn_plan **out);
+int spdnn_plan_sizes(const spdnn_plan *plan, spdnn_plan_sizes_t *sizes);
+/* Copy the plan into caller-owned host buffers sized from spdnn_plan_sizes:
+ *   blocks  int32[num_blocks * 8]  {first_group, num_groups, first_stage,
+ *                                   num_stages, first_seg_lo, first_seg_hi,
+ *                                   0, 0}
+ *   stages  int64[num_stages * 4]  {fp_offset, fp_count, rec_offset, rec_count}
+ *   segs    int32[num_segs * 2]    {record offset relative to its stage, count}
+ *   fp      int32[num_fp]          staged input neuron per smem slot
+ *   fpw     float[num_fp]          its weight (scaled form) or 1.0
+ *   rows    int32[num_groups * R]  output neuron per group row (-1 = padding)
+ *   records uint32[num_records * record_words]
+ *           word 0 = smem byte offset of the input neuron's tile row,
+ *           words 1..R = fp32 weight bits per group row (0 = not connected);
+ *           in the scaled form 1.0 / 0.0 connection masks
+ */
+int spdnn_plan_export(const spdnn_plan *plan, int32_t *blocks, int64_t *stages,
+                      int32_t *segs, int32_t *fp, float *fpw, int32_t *rows,
+                      uint32_t *records);
+void spdnn_plan_free(spdnn_plan *plan);
+
+/* ---- device execution ---------------------------------------------------- */
+
+/* Device-resident plan of one layer (pointers into device memory). */
+typedef struct spdnn_layer_dev {
+  const int32_t *blocks;
+  const int64_t *stages;
+  const int32_t *segs;
+  const int32_t *fp;
+  const float *fpw;
+  const int32_t *rows;
+  const uint32_t *records;
+  int64_t num_blocks;
+  int32_t rows_per_group;
+  int32_t record_words;
+  int32_t max_fp_per_stage;
+  int32_t max_records_per_stage;
+  int32_t scaled;
+} spdnn_layer_dev;
+
+/* Per-inference scratch shared by every layer launch (device pointers). */
+typedef struct spdnn_scratch {
+  int32_t *tile_done;      /* [ceil(M_cap/64)] zero-initialised */
+  uint32_t *tile_alive;    /* [2*ceil(M_cap/64)] zero-initialised */
+  int32_t *work;           /* [num_layers] zero-initialised work counters */
+} spdnn_scratch;
+
+/* One layer over the active features (engine.run_layer_step, engine.py:145-170):
+ *   y_in   : float[N][ld]   neuron-major, the active feature j lives in column
+ *            a_in[j], j < *m_in
+ *   y_out  : float[N][ld]   output for active feature j in column j
+ *   a_out / cat_out : surviving output columns and their categories, appended
+ *            tile by tile (order across tiles is not fixed; categories are
+ *            sorted once at the end, as the reference sorts, parallel.py:427)
+ *   *m_out : incremented by the number of survivors (caller zeroes it)
+ * `work` points at this launch's zeroed work counter. */
+int spdnn_layer_forward(const spdnn_layer_dev *layer, const float *bias,
+                        const float *y_in, float *y_out, int64_t ld,
+                        const int32_t *a_in, const int64_t *cat_in,
+                        const int32_t *m_in, int32_t *a_out, int64_t *cat_out,
+                        int32_t *m_out, const spdnn_scratch *scratch,
+                        int32_t *work, void *stream);
+
+/* All layers back to back on `stream` (engine.infer's loop, engine.py:264-285).
+ * Buffers ping-pong between index 0 and 1; counts[l] = active features
+ * entering layer l (counts[0] must hold M_0; counts[1..L] zeroed by caller).
+ * The final state is in buffer (num_layers % 2). */
+int spdnn_infer_layers(int64_t num_layers, const spdnn_layer_dev *layers,
+                       const float *bias, float *y0, float *y1, int64_t ld,
+                       int32_t *a0, int32_t *a1, int64_t *cat0, int64_t *cat1,
+                       int32_t *counts, const spdnn_scratch *scratch,
+                       void *stream);
+
+/* x: float[m][n] feature-major (FeatureBatch.data bytes) -> y: float[n][ld]. */
+int spdnn_transpose_in(const float *x, int64_t n, int64_t m, float *y,
+                       int64_t ld, void *stream);
+/* out[k][:] = y[:, a[perm[k]]] for k < m (feature-major result, i.e. the
+ * (N, m) Fortran FeatureBatch layout). perm may be NULL (identity). */
+int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int32_t *a,
+                     const int64_t *perm, int64_t m, float *out, void *stream);
+
+/* Threadblocks per SM the layer kernel runs with (for diagnostics). */
+int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_sm,
+                          int32_t *threads_per_cta);
+
+const char *spdnn_last_error(void);
+const char *spdnn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPDNN_B200_H */

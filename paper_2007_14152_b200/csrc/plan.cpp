@@ -1,0 +1,416 @@
+// plan.cpp -- one-time host conversion of a CSR layer into the B200 layout
+// ("row-grouped union ELL"). Replaces the reference's staging plan + sliced
+// ELL builders (spdnn/preprocess.py:148-190 build_staging_plan,
+// :212-244 csr_to_sliced_ell) as called from engine.prepare_layer
+// (spdnn/engine.py:77-85).
+//
+// Layout:
+//   * rows are put in an order where consecutive rows share many input
+//     columns (greedy nearest-overlap chain over the column->row index;
+//     generic, no knowledge of how the network was generated);
+//   * R consecutive rows form a group; the group's union U of input columns
+//     (ascending neuron index) becomes one "record" per column: the staged
+//     smem offset of that input neuron plus R weights (0 where a row does not
+//     connect). Every row still visits its own columns in ascending order,
+//     interleaved with exact +0 contributions, so its fp32 sum is bit-equal to
+//     the reference's ascending CSR sum (spdnn/kernels.py:27-37);
+//   * consecutive groups form a block whose input footprint (union of the
+//     group unions) is staged once per 64-feature tile; a block whose single
+//     group needs more than `footprint_cap` inputs is split into stages
+//     (the reference's buffer_capacity stages, preprocess.py:148-190).
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.h"
+
+struct spdnn_plan {
+  int64_t n = 0;
+  int R = 1, RW = 2;
+  std::vector<int32_t> blocks;   // 8 ints per block
+  std::vector<int64_t> stages;   // 4 per stage
+  std::vector<int32_t> segs;     // 2 per seg
+  std::vector<int32_t> fp;
+  std::vector<float> fpw;        // per staged neuron: its (column-uniform) weight
+  std::vector<int32_t> rows;
+  std::vector<uint32_t> records;
+  int64_t nnz = 0;
+  int64_t num_groups = 0;
+  int32_t max_fp = 0, max_rec = 0;
+  int32_t scaled = 0;            // 1: records hold 0/1 masks, staging scales by fpw
+};
+
+namespace {
+
+constexpr int kTileBytes = 64 * 4;  // one staged input neuron: 64 fp32 features
+
+int record_words(int R) { return R == 1 ? 2 : (R == 3 ? 4 : 8); }
+
+bool valid_csr(int64_t n, const int64_t *rp, const int32_t *ci) {
+  if (n < 0 || rp[0] != 0) return false;
+  for (int64_t r = 0; r < n; r++) {
+    if (rp[r + 1] < rp[r]) return false;
+    for (int64_t p = rp[r]; p < rp[r + 1]; p++) {
+      if (ci[p] < 0 || ci[p] >= n) return false;
+      if (p > rp[r] && ci[p] <= ci[p - 1]) return false;
+    }
+  }
+  return true;
+}
+
+// Greedy nearest-overlap chain: from the current row go to the unvisited row
+// sharing the most input columns (ties -> lower index); when none shares a
+// column, restart at the lowest unvisited row. Columns feeding more than
+// `deg_cap` rows are skipped as candidate generators (bounded cost on dense
+// columns; they still count toward nothing else).
+std::vector<int32_t> overlap_order(int64_t n, const int64_t *rp, const int32_t *ci) {
+  std::vector<int32_t> order;
+  order.reserve(n);
+  if (n == 0) return order;
+  // column -> rows (CSC pattern)
+  std::vector<int64_t> cp(n + 1, 0);
+  for (int64_t p = 0; p < rp[n]; p++) cp[ci[p] + 1]++;
+  for (int64_t c = 0; c < n; c++) cp[c + 1] += cp[c];
+  std::vector<int32_t> cr(rp[n]);
+  {
+    std::vector<int64_t> fill(cp.begin(), cp.end() - 1);
+    for (int64_t r = 0; r < n; r++)
+      for (int64_t p = rp[r]; p < rp[r + 1]; p++) cr[fill[ci[p]]++] = (int32_t)r;
+  }
+  const int64_t deg_cap = 512;
+  std::vector<uint8_t> visited(n, 0);
+  std::vector<int32_t> cnt(n, 0);
+  std::vector<int32_t> touched;
+  touched.reserve(4096);
+  int64_t next_free = 0;
+  int64_t cur = 0;
+  while ((int64_t)order.size() < n) {
+    if (cur < 0) {
+      while (visited[next_free]) next_free++;
+      cur = next_free;
+    }
+    visited[cur] = 1;
+    order.push_back((int32_t)cur);
+    int64_t best = -1;
+    int32_t bestc = 0;
+    for (int64_t p = rp[cur]; p < rp[cur + 1]; p++) {
+      int64_t c = ci[p];
+      if (cp[c + 1] - cp[c] > deg_cap) continue;
+      for (int64_t q = cp[c]; q < cp[c + 1]; q++) {
+        int32_t r2 = cr[q];
+        if (visited[r2]) continue;
+        if (cnt[r2]++ == 0) touched.push_back(r2);
+      }
+    }
+    for (int32_t r2 : touched) {
+      int32_t k = cnt[r2];
+      if (k > bestc || (k == bestc && r2 < best)) { bestc = k; best = r2; }
+      cnt[r2] = 0;
+    }
+    touched.clear();
+    cur = best;
+  }
+  return order;
+}
+
+// True when every stored weight of each input column is the same value, so the
+// product y[c]*w[c] can be formed once per staged neuron instead of once per
+// (row, column). Bit-exact either way: the same fp32 product is added.
+bool column_uniform(int64_t n, const int64_t *rp, const int32_t *ci, const float *va,
+                    std::vector<float> &colw) {
+  colw.assign(n, 0.0f);
+  std::vector<uint8_t> seen(n, 0);
+  for (int64_t p = 0; p < rp[n]; p++) {
+    int32_t c = ci[p];
+    uint32_t a, b;
+    std::memcpy(&a, &va[p], 4);
+    if (!seen[c]) { seen[c] = 1; colw[c] = va[p]; continue; }
+    std::memcpy(&b, &colw[c], 4);
+    if (a != b) return false;
+  }
+  return true;
+}
+
+struct Group {
+  int32_t rows[7];
+  std::vector<int32_t> cols;  // ascending union
+};
+
+// Union of the group's rows, ascending (k-way merge via sort of the <= 7*K cols).
+void group_union(const int64_t *rp, const int32_t *ci, const int32_t *rows, int R,
+                 std::vector<int32_t> &out) {
+  out.clear();
+  for (int k = 0; k < R; k++) {
+    if (rows[k] < 0) continue;
+    out.insert(out.end(), ci + rp[rows[k]], ci + rp[rows[k] + 1]);
+  }
+  std::sort(out.begin(), out.end());
+  out.erase(std::unique(out.begin(), out.end()), out.end());
+}
+
+std::vector<Group> make_groups(int64_t n, const int64_t *rp, const int32_t *ci,
+                               const std::vector<int32_t> &order, int R) {
+  std::vector<Group> gs((n + R - 1) / R);
+  for (size_t g = 0; g < gs.size(); g++) {
+    for (int k = 0; k < 7; k++) gs[g].rows[k] = -1;
+    for (int k = 0; k < R; k++) {
+      int64_t i = (int64_t)g * R + k;
+      if (i < n) gs[g].rows[k] = order[i];
+    }
+    group_union(rp, ci, gs[g].rows, R, gs[g].cols);
+  }
+  return gs;
+}
+
+int64_t total_records(const std::vector<Group> &gs) {
+  int64_t s = 0;
+  for (auto &g : gs) s += (int64_t)g.cols.size();
+  return s;
+}
+
+// Issue-slot / smem-wavefront cost per union record, per warp:
+// R=1: 4 issue, 3 wavefronts; R=3: 8 issue, 3 wavefronts; R=7: 17 issue,
+// 4 wavefronts. Time ~ max(issue/4, wavefronts) smem-or-issue bound per SM.
+double record_cost(int R) { return R == 1 ? 3.0 : (R == 3 ? 3.0 : 4.25); }
+
+void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
+          const std::vector<Group> &gs, const spdnn_plan_params &p,
+          const std::vector<float> *colw) {
+  const int R = pl->R, RW = pl->RW;
+  const int64_t n = pl->n;
+  const int S = p.footprint_cap, RC = p.record_cap, GMAX = p.max_groups;
+  std::vector<int32_t> stamp(n, -1);
+  std::vector<int32_t> slot_of(n, 0);
+  std::vector<int32_t> fp_block;
+  int32_t blk_id = 0;
+  // weight lookup for one row and column: rows are sorted, use binary search
+  auto weight = [&](int32_t row, int32_t col) -> float {
+    const int32_t *b = ci + rp[row], *e = ci + rp[row + 1];
+    const int32_t *it = std::lower_bound(b, e, col);
+    return (it != e && *it == col) ? va[it - ci] : 0.0f;
+  };
+  auto connected = [&](int32_t row, int32_t col) -> bool {
+    const int32_t *b = ci + rp[row], *e = ci + rp[row + 1];
+    const int32_t *it = std::lower_bound(b, e, col);
+    return it != e && *it == col;
+  };
+  pl->rows.resize(gs.size() * R);
+  for (size_t g = 0; g < gs.size(); g++)
+    for (int k = 0; k < R; k++) pl->rows[g * R + k] = gs[g].rows[k];
+
+  size_t g = 0;
+  while (g < gs.size()) {
+    // ---- choose the block's groups
+    size_t g0 = g;
+    fp_block.clear();
+    int64_t recs = 0;
+    while (g < gs.size() && (int64_t)(g - g0) < GMAX) {
+      int64_t newc = 0;
+      for (int32_t c : gs[g].cols) newc += (stamp[c] != blk_id);
+      if (g > g0 && ((int64_t)fp_block.size() + newc > S ||
+                     recs + (int64_t)gs[g].cols.size() > RC))
+        break;
+      for (int32_t c : gs[g].cols)
+        if (stamp[c] != blk_id) { stamp[c] = blk_id; fp_block.push_back(c); }
+      recs += (int64_t)gs[g].cols.size();
+      g++;
+    }
+    size_t ng = g - g0;
+    std::sort(fp_block.begin(), fp_block.end());
+    // ---- stages: one unless a lone group overflows the caps
+    int64_t nfp = (int64_t)fp_block.size();
+    int64_t nst = 1;
+    if (nfp > S || recs > RC) nst = (nfp + S - 1) / S;  // ng == 1 here
+    if (nst > 1 && ng != 1) nst = 1;  // cannot happen by construction
+    int64_t first_stage = (int64_t)pl->stages.size() / 4;
+    int64_t first_seg = (int64_t)pl->segs.size() / 2;
+    int32_t *blk = nullptr;
+    pl->blocks.resize(pl->blocks.size() + 8, 0);
+    blk = pl->blocks.data() + pl->blocks.size() - 8;
+    blk[0] = (int32_t)g0;
+    blk[1] = (int32_t)ng;
+    blk[2] = (int32_t)first_stage;
+    blk[3] = (int32_t)nst;
+    blk[4] = (int32_t)(first_seg & 0xffffffff);
+    blk[5] = (int32_t)(first_seg >> 32);
+    for (int64_t s = 0; s < nst; s++) {
+      int64_t c_lo = s * S, c_hi = std::min<int64_t>(nfp, (s + 1) * S);
+      if (nst == 1) { c_lo = 0; c_hi = nfp; }
+      int64_t fp_off = (int64_t)pl->fp.size();
+      for (int64_t i = c_lo; i < c_hi; i++) {
+        pl->fp.push_back(fp_block[i]);
+        pl->fpw.push_back(colw ? (*colw)[fp_block[i]] : 1.0f);
+        slot_of[fp_block[i]] = (int32_t)(i - c_lo);
+      }
+      int64_t rec_off = (int64_t)pl->records.size() / RW;
+      const int32_t lo_col = c_hi > c_lo ? fp_block[c_lo] : 0;
+      const int32_t hi_col = c_hi > c_lo ? fp_block[c_hi - 1] : -1;
+      for (size_t gg = g0; gg < g0 + ng; gg++) {
+        int64_t seg_start = (int64_t)pl->records.size() / RW - rec_off;
+        int64_t cntr = 0;
+        for (int32_t c : gs[gg].cols) {
+          if (c < lo_col || c > hi_col) continue;
+          size_t base = pl->records.size();
+          pl->records.resize(base + RW, 0u);
+          pl->records[base] = (uint32_t)slot_of[c] * (uint32_t)kTileBytes;
+          for (int k = 0; k < R; k++) {
+            int32_t row = gs[gg].rows[k];
+            float w = row >= 0 ? weight(row, c) : 0.0f;
+            if (colw) w = (row >= 0 && connected(row, c)) ? 1.0f : 0.0f;
+            uint32_t bits;
+            std::memcpy(&bits, &w, 4);
+            pl->records[base + 1 + k] = bits;
+          }
+          cntr++;
+        }
+        pl->segs.push_back((int32_t)seg_start);
+        pl->segs.push_back((int32_t)cntr);
+      }
+      int64_t rec_cnt = (int64_t)pl->records.size() / RW - rec_off;
+      pl->stages.push_back(fp_off);
+      pl->stages.push_back(c_hi - c_lo);
+      pl->stages.push_back(rec_off);
+      pl->stages.push_back(rec_cnt);
+      pl->max_fp = std::max<int32_t>(pl->max_fp, (int32_t)(c_hi - c_lo));
+      pl->max_rec = std::max<int32_t>(pl->max_rec, (int32_t)rec_cnt);
+    }
+    blk_id++;
+  }
+}
+
+}  // namespace
+
+extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t *col_idx,
+                                const float *values, const spdnn_plan_params *params,
+                                spdnn_plan **out) {
+  if (!out || !params || n < 0 || (n > 0 && !row_ptr) ||
+      (n > 0 && row_ptr[n] > 0 && (!col_idx || !values)))
+    return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: null argument");
+  *out = nullptr;
+  spdnn_plan_params p = *params;
+  if (p.footprint_cap < 1 || p.max_groups < 1 || p.record_cap < p.footprint_cap)
+    return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: bad params");
+  if (p.rows_per_group != 0 && p.rows_per_group != 1 && p.rows_per_group != 3 &&
+      p.rows_per_group != 7)
+    return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: rows_per_group must be 0, 1, 3 or 7");
+  if (n > 0 && !valid_csr(n, row_ptr, col_idx))
+    return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: CSR is not canonical");
+  if ((int64_t)p.footprint_cap * kTileBytes >= (int64_t)1 << 32)
+    return spdnn_fail(SPDNN_ERANGE, "spdnn_plan_build: footprint cap too large");
+  spdnn_plan *pl = new (std::nothrow) spdnn_plan();
+  if (!pl) return spdnn_fail(SPDNN_ENOMEM, "spdnn_plan_build: out of memory");
+  pl->n = n;
+  pl->nnz = n > 0 ? row_ptr[n] : 0;
+  try {
+    std::vector<int32_t> ident(n);
+    for (int64_t i = 0; i < n; i++) ident[i] = (int32_t)i;
+    int R = p.rows_per_group;
+    std::vector<Group> best;
+    if (R == 1 || n == 0) {
+      R = 1;
+      best = make_groups(n, row_ptr, col_idx, ident, 1);
+    } else {
+      std::vector<int32_t> order = p.reorder ? overlap_order(n, row_ptr, col_idx) : ident;
+      if (R != 0) {
+        best = make_groups(n, row_ptr, col_idx, order, R);
+      } else {
+        double best_cost = 0;
+        for (int cand : {1, 3, 7}) {
+          auto gs = make_groups(n, row_ptr, col_idx, cand == 1 ? ident : order, cand);
+          double cost = (double)total_records(gs) * record_cost(cand);
+          if (best.empty() && cand == 1) { best = std::move(gs); R = 1; best_cost = cost; continue; }
+          if (cost < best_cost) { best = std::move(gs); R = cand; best_cost = cost; }
+        }
+      }
+    }
+    pl->R = R;
+    pl->RW = record_words(R);
+    pl->num_groups = (int64_t)best.size();
+    std::vector<float> colw;
+    bool uni = p.allow_scaled && n > 0 && column_uniform(n, row_ptr, col_idx, values, colw);
+    pl->scaled = uni ? 1 : 0;
+    emit(pl, row_ptr, col_idx, values, best, p, uni ? &colw : nullptr);
+  } catch (const std::bad_alloc &) {
+    delete pl;
+    return spdnn_fail(SPDNN_ENOMEM, "spdnn_plan_build: out of memory");
+  }
+  *out = pl;
+  return SPDNN_OK;
+}
+
+extern "C" int spdnn_plan_build_many(int64_t num_layers, int64_t n,
+                                     const int64_t *const *row_ptr,
+                                     const int32_t *const *col_idx,
+                                     const float *const *values,
+                                     const spdnn_plan_params *params, int32_t threads,
+                                     spdnn_plan **out) {
+  if (num_layers < 0 || !out) return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build_many: bad args");
+  for (int64_t l = 0; l < num_layers; l++) out[l] = nullptr;
+  if (threads < 1) threads = 1;
+  std::vector<int> rc(num_layers, 0);
+  std::vector<std::string> msg(num_layers);
+  std::vector<std::thread> pool;
+  std::atomic<int64_t> next{0};
+  auto worker = [&]() {
+    for (;;) {
+      int64_t l = next.fetch_add(1);
+      if (l >= num_layers) break;
+      rc[l] = spdnn_plan_build(n, row_ptr[l], col_idx[l], values[l], params, &out[l]);
+      if (rc[l]) msg[l] = spdnn_last_error();  // thread-local: copy before leaving
+    }
+  };
+  int nt = (int)std::min<int64_t>(threads, std::max<int64_t>(num_layers, 1));
+  for (int t = 1; t < nt; t++) pool.emplace_back(worker);
+  worker();
+  for (auto &th : pool) th.join();
+  for (int64_t l = 0; l < num_layers; l++)
+    if (rc[l] != 0) {
+      for (int64_t k = 0; k < num_layers; k++) { spdnn_plan_free(out[k]); out[k] = nullptr; }
+      std::string m = "layer " + std::to_string(l) + ": " + msg[l];
+      return spdnn_fail(rc[l], m.c_str());
+    }
+  return SPDNN_OK;
+}
+
+extern "C" int spdnn_plan_sizes(const spdnn_plan *pl, spdnn_plan_sizes_t *s) {
+  if (!pl || !s) return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_sizes: null argument");
+  s->neurons = pl->n;
+  s->rows_per_group = pl->R;
+  s->record_words = pl->RW;
+  s->num_blocks = (int64_t)pl->blocks.size() / 8;
+  s->num_stages = (int64_t)pl->stages.size() / 4;
+  s->num_groups = pl->num_groups;
+  s->num_segs = (int64_t)pl->segs.size() / 2;
+  s->num_fp = (int64_t)pl->fp.size();
+  s->num_records = (int64_t)pl->records.size() / pl->RW;
+  s->nnz = pl->nnz;
+  s->padded_slots = s->num_records * pl->R;
+  s->max_fp_per_stage = pl->max_fp;
+  s->max_records_per_stage = pl->max_rec;
+  s->scaled = pl->scaled;
+  return SPDNN_OK;
+}
+
+extern "C" int spdnn_plan_export(const spdnn_plan *pl, int32_t *blocks, int64_t *stages,
+                                 int32_t *segs, int32_t *fp, float *fpw, int32_t *rows,
+                                 uint32_t *records) {
+  if (!pl) return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_export: null plan");
+  auto cp = [](auto *dst, const auto &v) {
+    if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+  };
+  cp(blocks, pl->blocks);
+  cp(stages, pl->stages);
+  cp(segs, pl->segs);
+  cp(fp, pl->fp);
+  cp(fpw, pl->fpw);
+  cp(rows, pl->rows);
+  cp(records, pl->records);
+  return SPDNN_OK;
+}
+
+extern "C" void spdnn_plan_free(spdnn_plan *pl) { delete pl; }

@@ -1,0 +1,574 @@
+"""Single-GPU inference engine: the drop-in for ``spdnn.engine``.
+
+Public surface and semantics follow ``spdnn/engine.py`` (paths relative to
+/root/reference/pkg/src/):
+
+* ``prepare_model(model, config, mode)``  <- engine.py:88-90 (one-time layout
+  conversion, here the C++ plan builder behind the C ABI);
+* ``infer(model, inputs, config, mode, prepared)`` <- engine.py:235-290;
+* ``optimized_layer`` / ``baseline_layer`` <- engine.py:93-127 (one layer,
+  returns the dense (N, M) output and per-column activity);
+* ``compact_active`` <- engine.py:130-142; ``run_layer_step`` <- :145-170;
+* ``LayerOutcome`` / ``InferenceResult`` / ``PreparedLayer`` <- :41-74.
+
+Both modes run the same sm_100a kernel (csrc/layer.cu). "optimized" uses
+row-grouped union plans (R = 3 or 7 rows share every staged operand);
+"baseline" uses one row per group (R = 1), i.e. each output row gathers only
+its own columns -- the analogue of the reference's CSR baseline kernel. The
+two produce bit-identical outputs, as in the reference (kernels.py:1-9).
+
+Device data layout: features are neuron-major,
+``Y[n][j]`` with the 64-feature tiles contiguous, so every staged input
+neuron is one coalesced 256-byte row segment; dead features are dropped by
+index lists that the layer kernel itself appends (no compaction pass).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+import time
+from dataclasses import dataclass, field, replace
+from typing import Literal, Sequence
+
+import numpy as np
+
+from . import _native
+from .model import (FeatureBatch, InferenceConfig, LayerCSR, ModelError, NetworkModel,
+                    count_edges)
+
+Mode = Literal["baseline", "optimized"]
+TILE = 64
+
+
+# ---------------------------------------------------------------------------
+# result types (engine.py:41-65)
+
+@dataclass
+class LayerOutcome:
+    active_before: int
+    active_after: int
+    weight_element_reads: int
+    feature_element_reads: int
+    features: FeatureBatch | None = None
+
+    def summary(self) -> "LayerOutcome":
+        return replace(self, features=None)
+
+
+@dataclass
+class InferenceResult:
+    final: FeatureBatch
+    categories: np.ndarray  # sorted int64
+    per_layer: list
+    elapsed_seconds: float
+    edges_processed: int
+    device_seconds: float = 0.0   # CUDA-event time of the layer loop alone
+
+
+# ---------------------------------------------------------------------------
+# one-time layout conversion
+
+@dataclass(frozen=True)
+class PlanParams:
+    """Kernel geometry knobs of the row-grouped union layout."""
+    rows_per_group: int = 0      # 0 = cost model picks 1, 3 or 7 per layer
+    footprint_cap: int = 192     # staged input neurons per block stage (x256 B smem)
+    max_groups: int = 16         # row groups per block (one per warp)
+    record_cap: int = 1024       # union records per block stage
+    reorder: bool = True
+    allow_scaled: bool = True
+
+
+BASELINE_PARAMS = PlanParams(rows_per_group=1, reorder=False, allow_scaled=False)
+OPTIMIZED_PARAMS = PlanParams()
+
+
+@dataclass(frozen=True)
+class PaddingStats:
+    """Union-padding cost of the layout: multiply-add slots vs nonzeros."""
+    nnz: int
+    padded_slots: int      # records * R (slots executed per feature)
+    overhead: float        # (padded_slots - nnz) / nnz
+    empty: bool = False
+
+
+@dataclass(frozen=True)
+class LayerPlan:
+    """Host copy of one layer's device layout (include/spdnn_b200.h export)."""
+    neurons: int
+    rows_per_group: int
+    record_words: int
+    scaled: bool
+    num_blocks: int
+    max_fp_per_stage: int
+    max_records_per_stage: int
+    num_records: int
+    num_fp: int
+    blocks: np.ndarray
+    stages: np.ndarray
+    segs: np.ndarray
+    fp: np.ndarray
+    fpw: np.ndarray
+    rows: np.ndarray
+    records: np.ndarray
+
+    @property
+    def total_slots(self) -> int:
+        return self.num_records * self.rows_per_group
+
+
+@dataclass(frozen=True)
+class PreparedLayer:
+    """Execution-ready structures for one layer in one mode (engine.py:68-74)."""
+    csr: LayerCSR
+    plan: LayerPlan | None = None
+    padding: PaddingStats | None = None
+    mode: str = "optimized"
+
+
+def _params_struct(p: PlanParams) -> _native.PlanParams:
+    return _native.PlanParams(p.rows_per_group, p.footprint_cap, p.max_groups, p.record_cap,
+                              int(p.reorder), int(p.allow_scaled))
+
+
+def _export(handle) -> LayerPlan:
+    L = _native.lib()
+    s = _native.PlanSizes()
+    _native.check(L.spdnn_plan_sizes(handle, ctypes.byref(s)), "spdnn_plan_sizes")
+    arrs = dict(
+        blocks=np.zeros(s.num_blocks * 8, np.int32),
+        stages=np.zeros(s.num_stages * 4, np.int64),
+        segs=np.zeros(s.num_segs * 2, np.int32),
+        fp=np.zeros(s.num_fp, np.int32),
+        fpw=np.zeros(s.num_fp, np.float32),
+        rows=np.zeros(s.num_groups * s.rows_per_group, np.int32),
+        records=np.zeros(s.num_records * s.record_words, np.uint32),
+    )
+    ptr = lambda a: ctypes.c_void_p(a.ctypes.data)
+    _native.check(L.spdnn_plan_export(handle, ptr(arrs["blocks"]), ptr(arrs["stages"]),
+                                      ptr(arrs["segs"]), ptr(arrs["fp"]), ptr(arrs["fpw"]),
+                                      ptr(arrs["rows"]), ptr(arrs["records"])),
+                  "spdnn_plan_export")
+    return LayerPlan(neurons=s.neurons, rows_per_group=s.rows_per_group,
+                     record_words=s.record_words, scaled=bool(s.scaled),
+                     num_blocks=s.num_blocks, max_fp_per_stage=s.max_fp_per_stage,
+                     max_records_per_stage=s.max_records_per_stage,
+                     num_records=s.num_records, num_fp=s.num_fp, **arrs)
+
+
+def _padding(layer: LayerCSR, plan: LayerPlan) -> PaddingStats:
+    nnz = layer.nnz
+    if nnz == 0:
+        return PaddingStats(0, plan.total_slots, 0.0, empty=True)
+    return PaddingStats(nnz, plan.total_slots, (plan.total_slots - nnz) / nnz)
+
+
+def build_plans(layers: Sequence[LayerCSR], params: PlanParams, threads: int = 0) -> list:
+    """C++ conversion of many layers on host threads (spdnn_plan_build_many)."""
+    L = _native.lib()
+    n_layers = len(layers)
+    if n_layers == 0:
+        return []
+    n = layers[0].neurons
+    keep = []
+    rps = (ctypes.c_void_p * n_layers)()
+    cis = (ctypes.c_void_p * n_layers)()
+    vas = (ctypes.c_void_p * n_layers)()
+    for i, lay in enumerate(layers):
+        if lay.neurons != n:
+            raise ModelError("all layers must have the same neuron count")
+        keep.append(lay)
+        rps[i] = lay.row_ptr.ctypes.data
+        cis[i] = lay.col_idx.ctypes.data if lay.nnz else 0
+        vas[i] = lay.values.ctypes.data if lay.nnz else 0
+    handles = (ctypes.c_void_p * n_layers)()
+    if threads <= 0:
+        import os
+        threads = min(32, os.cpu_count() or 1)
+    pp = _params_struct(params)
+    _native.check(L.spdnn_plan_build_many(n_layers, n, rps, cis, vas, ctypes.byref(pp),
+                                          int(threads), handles), "prepare_model")
+    try:
+        return [_export(handles[i]) for i in range(n_layers)]
+    finally:
+        for i in range(n_layers):
+            L.spdnn_plan_free(handles[i])
+
+
+def prepare_layer(layer: LayerCSR, config: InferenceConfig, mode: Mode) -> PreparedLayer:
+    return prepare_model(NetworkModel(layer.neurons, (layer,), np.zeros(layer.neurons)),
+                         config, mode)[0]
+
+
+def prepare_model(model: NetworkModel, config: InferenceConfig, mode: Mode,
+                  params: PlanParams | None = None) -> list:
+    """One-time conversion of every layer (engine.py:88-90), outside any clock."""
+    if mode not in ("baseline", "optimized"):
+        raise ModelError(f"unknown mode {mode!r}")
+    if params is None:
+        params = BASELINE_PARAMS if mode == "baseline" else OPTIMIZED_PARAMS
+    plans = build_plans(model.layers, params)
+    return [PreparedLayer(csr=lay, plan=pl, padding=_padding(lay, pl), mode=mode)
+            for lay, pl in zip(model.layers, plans)]
+
+
+# ---------------------------------------------------------------------------
+# device residency
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2007_14152_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return torch
+
+
+def _dptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(torch) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class DeviceNetwork:
+    """All layer plans of a network resident in HBM, plus the bias vector.
+
+    Arrays of all layers are concatenated per kind (one allocation each);
+    ``layer_devs`` holds one ``spdnn_layer_dev`` per layer pointing into them.
+    """
+
+    def __init__(self, prepared: Sequence[PreparedLayer], bias: np.ndarray, device=None):
+        torch = _torch()
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.num_layers = len(prepared)
+        self.neurons = int(bias.shape[0])
+        self.modes = {p.mode for p in prepared}
+        plans = [p.plan for p in prepared]
+        kinds = ("blocks", "stages", "segs", "fp", "fpw", "rows", "records")
+        self.buffers = {}
+        offsets = {k: [] for k in kinds}
+        for k in kinds:
+            parts = [getattr(pl, k) for pl in plans]
+            off = 0
+            for a in parts:
+                offsets[k].append(off)
+                off += a.shape[0]
+            cat = np.concatenate(parts) if parts else np.zeros(0, np.int32)
+            if cat.dtype == np.uint32:
+                cat = cat.view(np.int32)
+            if cat.size == 0:
+                cat = np.zeros(1, dtype=cat.dtype)
+            self.buffers[k] = torch.from_numpy(np.ascontiguousarray(cat)).to(self.device)
+        self.bias = torch.from_numpy(np.ascontiguousarray(bias, np.float32)).to(self.device)
+        self.layer_devs = (_native.LayerDev * max(1, self.num_layers))()
+        self.max_fp = 0
+        for l, pl in enumerate(plans):
+            d = self.layer_devs[l]
+            for k in kinds:
+                buf = self.buffers[k]
+                setattr(d, k, buf.data_ptr() + offsets[k][l] * buf.element_size())
+            d.num_blocks = pl.num_blocks
+            d.rows_per_group = pl.rows_per_group
+            d.record_words = pl.record_words
+            d.max_fp_per_stage = pl.max_fp_per_stage
+            d.max_records_per_stage = pl.max_records_per_stage
+            d.scaled = int(pl.scaled)
+        self.total_slots = [pl.total_slots for pl in plans]
+        self.num_fp = [pl.num_fp for pl in plans]
+        self.hbm_bytes = sum(int(b.numel() * b.element_size()) for b in self.buffers.values())
+
+
+class Workspace:
+    """Per-inference device buffers for a feature-count capacity (reused)."""
+
+    def __init__(self, neurons: int, m_cap: int, num_layers: int, device):
+        torch = _torch()
+        self.neurons = neurons
+        self.m_cap = m_cap
+        self.ld = max(TILE, -(-m_cap // TILE) * TILE)
+        self.num_layers = num_layers
+        f32, i32, i64 = torch.float32, torch.int32, torch.int64
+        self.x = torch.empty((m_cap, neurons), dtype=f32, device=device)  # raw upload
+        self.y = [torch.empty((neurons, self.ld), dtype=f32, device=device) for _ in range(2)]
+        self.a = [torch.empty(self.ld, dtype=i32, device=device) for _ in range(2)]
+        self.cat = [torch.empty(self.ld, dtype=i64, device=device) for _ in range(2)]
+        self.counts = torch.zeros(num_layers + 1, dtype=i32, device=device)
+        tiles = self.ld // TILE
+        self.tile_done = torch.zeros(tiles, dtype=i32, device=device)
+        self.tile_alive = torch.zeros(2 * tiles, dtype=i32, device=device)
+        self.work = torch.zeros(max(1, num_layers), dtype=i32, device=device)
+        self.scratch = _native.Scratch(self.tile_done.data_ptr(), self.tile_alive.data_ptr(),
+                                       self.work.data_ptr())
+        self.iota = torch.arange(self.ld, dtype=i32, device=device)
+
+    def fits(self, neurons: int, m: int, num_layers: int) -> bool:
+        return neurons == self.neurons and m <= self.m_cap and num_layers <= self.num_layers
+
+
+_cache_lock = threading.Lock()
+_net_cache: dict = {}
+_ws_cache: dict = {}
+
+
+def device_network(prepared: Sequence[PreparedLayer], bias: np.ndarray) -> DeviceNetwork:
+    """Upload (once) and cache the device copy of a prepared model. One
+    network stays resident per process: a new one evicts the previous."""
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    with _cache_lock:
+        hit = _net_cache.get("net")
+        if hit is not None:
+            c_prep, c_bias, c_dev, net = hit
+            if c_prep is prepared and c_dev == dev and np.array_equal(c_bias, bias):
+                return net
+        _net_cache.clear()
+        net = DeviceNetwork(prepared, bias)
+        _net_cache["net"] = (prepared, np.array(bias, copy=True), dev, net)
+        return net
+
+
+def workspace(neurons: int, m: int, num_layers: int) -> Workspace:
+    torch = _torch()
+    dev = torch.cuda.current_device()
+    key = (dev, threading.get_ident())
+    with _cache_lock:
+        ws = _ws_cache.get(key)
+        if ws is None or not ws.fits(neurons, m, num_layers):
+            ws = None
+            _ws_cache.pop(key, None)
+            torch.cuda.empty_cache()
+            ws = Workspace(neurons, max(m, 1), num_layers, torch.device("cuda", dev))
+            _ws_cache[key] = ws
+        return ws
+
+
+# ---------------------------------------------------------------------------
+# device execution
+
+class DeviceRun:
+    """State of one on-device inference after the layer loop."""
+
+    def __init__(self, ws: Workspace, num_layers: int, m0: int):
+        self.ws = ws
+        self.num_layers = num_layers
+        self.m0 = m0
+        self.out_index = num_layers % 2
+
+
+def stage_inputs(ws: Workspace, x_host_or_dev, categories, stream=None) -> None:
+    """Copy (M, N) feature-major inputs into the workspace and lay them out
+    neuron-major (spdnn_transpose_in); A = 0..M-1; categories as given."""
+    torch = _torch()
+    m = int(x_host_or_dev.shape[0])
+    n = ws.neurons
+    if m:
+        ws.x[:m].copy_(x_host_or_dev, non_blocking=True)
+        _native.check(_native.lib().spdnn_transpose_in(_dptr(ws.x), n, m, _dptr(ws.y[0]), ws.ld,
+                                                      _stream_ptr(torch)), "spdnn_transpose_in")
+        ws.a[0][:m].copy_(ws.iota[:m])
+        ws.cat[0][:m].copy_(categories, non_blocking=True)
+
+
+def run_layers(net: DeviceNetwork, ws: Workspace, m0: int) -> DeviceRun:
+    """Enqueue every layer on the current stream; no host synchronisation."""
+    torch = _torch()
+    ws.counts.zero_()
+    ws.counts[0] = m0
+    ws.work.zero_()
+    _native.check(_native.lib().spdnn_infer_layers(
+        net.num_layers, net.layer_devs, _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
+        _dptr(ws.a[0]), _dptr(ws.a[1]), _dptr(ws.cat[0]), _dptr(ws.cat[1]), _dptr(ws.counts),
+        ctypes.byref(ws.scratch), _stream_ptr(torch)), "spdnn_infer_layers")
+    return DeviceRun(ws, net.num_layers, m0)
+
+
+def collect(run: DeviceRun, want_values: bool = True):
+    """Sorted survivor categories (+ their values as (S, N) feature-major) and
+    the per-layer active counts. One host synchronisation."""
+    torch = _torch()
+    ws = run.ws
+    counts = ws.counts[: run.num_layers + 1].cpu().numpy().astype(np.int64)
+    s = int(counts[run.num_layers]) if run.num_layers else run.m0
+    o = run.out_index
+    cats = ws.cat[o][:s]
+    sorted_cats, perm = torch.sort(cats)
+    values = None
+    if want_values:
+        out = torch.empty((s, ws.neurons), dtype=torch.float32, device=ws.y[o].device)
+        _native.check(_native.lib().spdnn_gather_out(
+            _dptr(ws.y[o]), ws.neurons, ws.ld, _dptr(ws.a[o]), _dptr(perm), s, _dptr(out),
+            _stream_ptr(torch)), "spdnn_gather_out")
+        values = out
+    return counts, sorted_cats, values
+
+
+def _check_inputs(model: NetworkModel, inputs: FeatureBatch, mode) -> None:
+    if inputs.neurons != model.neurons:
+        raise ModelError("inputs do not match model width")
+    if mode not in ("baseline", "optimized"):
+        raise ModelError(f"unknown mode {mode!r}")
+
+
+def _check_prepared(prepared: Sequence[PreparedLayer], model: NetworkModel, mode) -> None:
+    if len(prepared) != model.num_layers:
+        raise ModelError("prepared structures do not match the model depth")
+    for p in prepared:
+        if p.plan is None or p.mode != mode:
+            raise ModelError(f"prepared structures are for {p.mode} mode")
+
+
+def _outcomes(counts: np.ndarray, net: DeviceNetwork) -> list:
+    outs = []
+    for l in range(net.num_layers):
+        before, after = int(counts[l]), int(counts[l + 1])
+        if before == 0:
+            outs.append(LayerOutcome(0, 0, 0, 0))
+            continue
+        tiles = -(-before // TILE)
+        outs.append(LayerOutcome(active_before=before, active_after=after,
+                                 weight_element_reads=net.total_slots[l] * tiles,
+                                 feature_element_reads=net.num_fp[l] * before))
+    return outs
+
+
+def infer(model: NetworkModel, inputs: FeatureBatch, config: InferenceConfig,
+          mode: Mode = "optimized", prepared: Sequence[PreparedLayer] | None = None,
+          values: bool = True) -> InferenceResult:
+    """All layers with pruning after each (engine.py:235-290), on the GPU.
+
+    The clock covers the layer loop only, like the reference's (prepare and
+    result assembly excluded); ``device_seconds`` is the same span measured
+    with CUDA events. ``values=False`` (extension) skips copying the final
+    feature values back: ``final`` is then None and only the sorted
+    categories and per-layer counts come back -- the Graph Challenge output.
+    """
+    _check_inputs(model, inputs, mode)
+    if config.streaming and prepared is not None:
+        raise ModelError("prepared structures cannot be combined with streaming")
+    if prepared is None:
+        prepared = prepare_model(model, config, mode)
+    _check_prepared(prepared, model, mode)
+    torch = _torch()
+    n, m = model.neurons, inputs.active_count
+    if model.num_layers == 0 or m == 0:
+        per = [LayerOutcome(0, 0, 0, 0) for _ in range(model.num_layers)]
+        if m and model.num_layers == 0:
+            per = []
+        return InferenceResult(final=inputs, categories=inputs.categories.copy(),
+                               per_layer=per, elapsed_seconds=0.0,
+                               edges_processed=inputs.total_inputs * count_edges(model))
+    net = device_network(prepared, model.bias)
+    ws = workspace(n, m, model.num_layers)
+    x = torch.from_numpy(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
+    cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
+    stage_inputs(ws, x, cats)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev0.record()
+    run = run_layers(net, ws, m)
+    ev1.record()
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - t0
+    counts, sorted_cats, vals = collect(run, want_values=values)
+    cats_np = sorted_cats.cpu().numpy().astype(np.int64)
+    final = None
+    if values:
+        final = FeatureBatch(neurons=n, data=vals.cpu().numpy().T, categories=cats_np,
+                             total_inputs=inputs.total_inputs)
+    return InferenceResult(final=final, categories=cats_np.copy(),
+                           per_layer=_outcomes(counts, net), elapsed_seconds=elapsed,
+                           edges_processed=inputs.total_inputs * count_edges(model),
+                           device_seconds=ev0.elapsed_time(ev1) / 1e3)
+
+
+# ---------------------------------------------------------------------------
+# single-layer entry points (engine.py:93-127) and host helpers
+
+def _one_layer(features: FeatureBatch, prepared: PreparedLayer, bias: np.ndarray):
+    torch = _torch()
+    n, m = features.neurons, features.active_count
+    if m == 0:
+        return np.zeros((n, 0), np.float32, order="F"), np.zeros(0, bool)
+    net = DeviceNetwork([prepared], bias)
+    ws = Workspace(n, m, 1, torch.device("cuda", torch.cuda.current_device()))
+    x = torch.from_numpy(np.asarray(features.data).T)
+    stage_inputs(ws, x, torch.arange(m, dtype=torch.int64))
+    ws.counts.zero_()
+    ws.counts[0] = m
+    _native.check(_native.lib().spdnn_layer_forward(
+        ctypes.byref(net.layer_devs[0]), _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
+        _dptr(ws.a[0]), _dptr(ws.cat[0]), _dptr(ws.counts), _dptr(ws.a[1]), _dptr(ws.cat[1]),
+        ctypes.c_void_p(ws.counts.data_ptr() + 4), ctypes.byref(ws.scratch), _dptr(ws.work),
+        _stream_ptr(torch)), "spdnn_layer_forward")
+    out = torch.empty((m, n), dtype=torch.float32, device=ws.y[1].device)
+    _native.check(_native.lib().spdnn_gather_out(_dptr(ws.y[1]), n, ws.ld, _dptr(ws.iota),
+                                                 ctypes.c_void_p(0), m, _dptr(out),
+                                                 _stream_ptr(torch)), "spdnn_gather_out")
+    s = int(ws.counts[1].item())
+    alive = np.zeros(m, dtype=bool)
+    alive[ws.a[1][:s].cpu().numpy()] = True
+    return out.cpu().numpy().T, alive
+
+
+def optimized_layer(features: FeatureBatch, prepared, bias: np.ndarray,
+                    minibatch: int | None = None):
+    """One fused layer on the GPU; returns ((N, M) F-order out, active flags).
+
+    ``prepared`` is a PreparedLayer (or its LayerPlan). ``minibatch`` is
+    accepted for signature compatibility (engine.py:109); the kernel's feature
+    tile is fixed at 64.
+    """
+    if minibatch is not None and minibatch < 1:
+        raise ModelError("minibatch must be positive")
+    if isinstance(prepared, LayerPlan):
+        prepared = PreparedLayer(csr=None, plan=prepared)
+    if prepared.plan is None:
+        raise ModelError("prepared structures are for baseline mode")
+    n = prepared.plan.neurons
+    if features.neurons != n or len(bias) != n:
+        raise ModelError("dimension mismatch in optimized_layer")
+    return _one_layer(features, prepared, np.asarray(bias, np.float32))
+
+
+def baseline_layer(features: FeatureBatch, layer: LayerCSR, bias: np.ndarray):
+    """One layer with one row per group (each row gathers its own columns)."""
+    n = layer.neurons
+    if features.neurons != n or len(bias) != n:
+        raise ModelError("dimension mismatch in baseline_layer")
+    plan = build_plans([layer], BASELINE_PARAMS)[0]
+    return _one_layer(features, PreparedLayer(csr=layer, plan=plan, mode="baseline"),
+                      np.asarray(bias, np.float32))
+
+
+def compact_active(out: np.ndarray, active: np.ndarray, categories: np.ndarray,
+                   total_inputs: int | None = None) -> FeatureBatch:
+    """Keep only active columns with their categories (engine.py:130-142)."""
+    if len(active) != out.shape[1] or len(categories) != out.shape[1]:
+        raise ModelError("flag/category length must match column count")
+    categories = np.asarray(categories, dtype=np.int64)
+    if total_inputs is None:
+        total_inputs = int(categories.max()) + 1 if len(categories) else 0
+    return FeatureBatch(neurons=out.shape[0], data=np.asfortranarray(out[:, active]),
+                        categories=categories[active], total_inputs=total_inputs)
+
+
+def run_layer_step(features: FeatureBatch, prepared: PreparedLayer, bias: np.ndarray,
+                   config: InferenceConfig, mode: Mode) -> LayerOutcome:
+    """One evaluate-then-compact step (engine.py:145-170)."""
+    before = features.active_count
+    if before == 0:
+        return LayerOutcome(0, 0, 0, 0, features=features)
+    if prepared.plan is None or prepared.mode != mode:
+        raise ModelError(f"prepared structures are for {prepared.mode} mode")
+    out, active = _one_layer(features, prepared, np.asarray(bias, np.float32))
+    tiles = -(-before // TILE)
+    compacted = compact_active(out, active, features.categories,
+                               total_inputs=features.total_inputs)
+    return LayerOutcome(active_before=before, active_after=compacted.active_count,
+                        weight_element_reads=prepared.plan.total_slots * tiles,
+                        feature_element_reads=prepared.plan.num_fp * before,
+                        features=compacted)

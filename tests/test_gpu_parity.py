@@ -1,0 +1,203 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle and
+the reference fixtures. Integer/category results must be identical and, since
+the kernel keeps the reference's per-row ascending fp32 order, values are
+checked bit for bit as well (north-star tolerance 1e-4 is the fallback bound
+written next to each value check)."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, load_npz, random_layer
+from oracle import oracle
+from paper_2007_14152_b200 import engine, ingest
+from paper_2007_14152_b200.engine import PlanParams, build_plans
+from paper_2007_14152_b200.model import (InferenceConfig, LayerCSR, ModelError, NetworkModel,
+                                         make_feature_batch, make_layer_csr)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4  # north star: final values within 1e-4 absolute
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def same_bits(a, b):
+    a = np.asarray(a, np.float32)
+    b = np.asarray(b, np.float32)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def _layer_case(layer, params, rng, m):
+    n = layer.neurons
+    x = rng.uniform(0, 3, (n, m)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, n).astype(np.float32)
+    plan = build_plans([layer], params)[0]
+    prep = engine.PreparedLayer(csr=layer, plan=plan)
+    y, act = engine.optimized_layer(make_feature_batch(n, x), prep, bias)
+    ref, ref_act = oracle.layer(layer, bias, x)
+    assert same_bits(y, ref)
+    assert np.array_equal(act, ref_act)
+
+
+PARAMS = [PlanParams(), PlanParams(rows_per_group=1, reorder=False, allow_scaled=False),
+          PlanParams(rows_per_group=3), PlanParams(rows_per_group=7, allow_scaled=False),
+          PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3),
+          PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2)]
+
+
+@pytest.mark.parametrize("pi", range(len(PARAMS)))
+def test_layer_random_pm_weights(cuda_ok, pi):
+    rng = np.random.default_rng(7 + pi)
+    for _ in range(12):
+        n = int(rng.integers(1, 90))
+        layer = random_layer(rng, n, max_row_nnz=min(n, int(rng.integers(1, 16))))
+        _layer_case(layer, PARAMS[pi], rng, m=int(rng.integers(1, 200)))
+
+
+@pytest.mark.parametrize("pi", range(len(PARAMS)))
+def test_layer_synthetic(cuda_ok, pi):
+    rng = np.random.default_rng(70 + pi)
+    for n, k in ((64, 16), (1024, 32), (4096, 32), (1000, 7)):
+        model = ingest.generate_synthetic_network(
+            ingest.GeneratorSpec(neurons=n, layers=1, connections_per_neuron=k,
+                                 seed=int(rng.integers(1 << 30))))
+        _layer_case(model.layers[0], PARAMS[pi], rng, m=int(rng.integers(60, 300)))
+
+
+def test_layer_reference_fixtures(cuda_ok):
+    """Single layers whose expected outputs came from the reference itself."""
+    z = load_npz("layers.npz")
+    for i in range(int(z["count"])):
+        layer = LayerCSR(z[f"l{i}_row_ptr"], z[f"l{i}_col"], z[f"l{i}_val"])
+        feats = make_feature_batch(layer.neurons, z[f"l{i}_x"])
+        for mode_fn in (lambda: engine.baseline_layer(feats, layer, z[f"l{i}_bias"]),
+                        lambda: engine.optimized_layer(
+                            feats, engine.prepare_layer(layer, InferenceConfig(), "optimized"),
+                            z[f"l{i}_bias"])):
+            y, act = mode_fn()
+            assert same_bits(y, z[f"l{i}_y"]), i
+            assert np.array_equal(act, z[f"l{i}_active"]), i
+
+
+def test_layer_dense_multistage_rows(cuda_ok):
+    rng = np.random.default_rng(6)
+    n = 700
+    rows = np.repeat(np.arange(5), 600)
+    cols = np.concatenate([rng.choice(n, 600, replace=False) for _ in range(5)])
+    layer = make_layer_csr(n, rows, cols, rng.uniform(-1, 1, 3000).astype(np.float32))
+    for p in (PlanParams(rows_per_group=3), PlanParams(rows_per_group=1, reorder=False)):
+        _layer_case(layer, p, rng, m=130)
+
+
+@pytest.mark.parametrize("mode", ["optimized", "baseline"])
+def test_infer_reference_nets(cuda_ok, mode):
+    """60 whole networks with reference-produced categories, counts, values."""
+    z = load_npz("nets.npz")
+    for c in range(int(z["count"])):
+        n, L, k, m, mseed, iseed = (int(v) for v in z[f"c{c}_spec"])
+        model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+            neurons=n, layers=L, connections_per_neuron=k, bias_value=float(z[f"c{c}_bias"]),
+            seed=mseed))
+        inputs = ingest.generate_synthetic_inputs(n, m, float(z[f"c{c}_density"]), seed=iseed)
+        res = engine.infer(model, inputs, InferenceConfig(), mode=mode)
+        counts = [o.active_before for o in res.per_layer] + [res.per_layer[-1].active_after]
+        assert np.array_equal(res.categories, z[f"c{c}_cats"]), c
+        assert counts == z[f"c{c}_counts"].tolist(), c
+        assert same_bits(res.final.data, z[f"c{c}_final"]), c
+
+
+def test_infer_random_pm_networks_vs_oracle(cuda_ok):
+    rng = np.random.default_rng(31)
+    for _ in range(8):
+        n = int(rng.integers(8, 120))
+        L = int(rng.integers(1, 6))
+        layers = [random_layer(rng, n, max_row_nnz=min(n, 10)) for _ in range(L)]
+        bias = rng.uniform(-0.3, 0.3, n).astype(np.float32)
+        model = NetworkModel(neurons=n, layers=layers, bias=bias)
+        m = int(rng.integers(1, 300))
+        inputs = make_feature_batch(n, rng.uniform(0, 2, (n, m)).astype(np.float32))
+        ref = oracle.infer(model, inputs)
+        for mode in ("optimized", "baseline"):
+            res = engine.infer(model, inputs, InferenceConfig(), mode=mode)
+            assert np.array_equal(res.categories, ref.categories)
+            assert [o.active_before for o in res.per_layer] == ref.counts[:-1].tolist()
+            assert same_bits(res.final.data, ref.final)
+
+
+def test_flagship_digest(cuda_ok):
+    d = json.load(open(os.path.join(GOLDEN, "digests.json")))["flagship"]
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=120, connections_per_neuron=32, bias_value=-0.3, seed=1))
+    inputs = ingest.generate_synthetic_inputs(1024, 6000, 0.3, seed=2)
+    res = engine.infer(model, inputs, InferenceConfig())
+    counts = [o.active_before for o in res.per_layer] + [res.per_layer[-1].active_after]
+    assert len(res.categories) == d["survivors"]
+    assert sha(res.categories.astype("<i8")) == d["categories_sha256"]
+    assert counts == d["counts"]
+    assert sha(np.asarray(res.final.data, dtype="<f4").T) == d["final_sha256"]
+
+
+def test_config1_full_digest(cuda_ok):
+    """BASELINE.json config 1 at full size (60000 inputs): exact categories and
+    the exact per-layer active-count sequence of the reference."""
+    d = json.load(open(os.path.join(GOLDEN, "digests.json")))["config1"]
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=120, connections_per_neuron=32, bias_value=-0.3, seed=1))
+    inputs = ingest.generate_synthetic_inputs(1024, 60000, 0.3, seed=2)
+    res = engine.infer(model, inputs, InferenceConfig())
+    counts = np.array([o.active_before for o in res.per_layer] +
+                      [res.per_layer[-1].active_after], np.int64)
+    assert len(res.categories) == d["survivors"]
+    assert sha(res.categories.astype("<i8")) == d["categories_sha256"]
+    assert sha(counts.astype("<i8")) == d["counts_sha256"]
+    assert int(counts[:-1].sum()) == d["sum_active"]
+    assert (res.final.data == 32.0).all()  # every final value is 32.0
+
+
+def test_edge_cases(cuda_ok):
+    # zero layers: identity (tests/test_engine.py:87-93)
+    model = NetworkModel(neurons=4, layers=(), bias=np.zeros(4))
+    inputs = make_feature_batch(4, np.ones((4, 3), np.float32))
+    res = engine.infer(model, inputs, InferenceConfig())
+    assert res.categories.tolist() == [0, 1, 2] and res.per_layer == []
+    # all-zero inputs die in layer 0; later layers report zeros (engine.py:265-270)
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=32, layers=5, connections_per_neuron=4, bias_value=-0.3, seed=2))
+    res = engine.infer(model, make_feature_batch(32, np.zeros((32, 6), np.float32)),
+                       InferenceConfig())
+    assert res.categories.tolist() == []
+    assert res.per_layer[0].active_before == 6 and res.per_layer[0].active_after == 0
+    assert res.per_layer[0].weight_element_reads > 0
+    assert all(o.active_before == 0 for o in res.per_layer[1:])
+    # one neuron, one feature, m not a multiple of 64, categories carried through
+    layer = make_layer_csr(1, np.array([0]), np.array([0]), np.array([2.0], np.float32))
+    m1 = NetworkModel(neurons=1, layers=(layer,), bias=np.array([-1.0], np.float32))
+    res = engine.infer(m1, make_feature_batch(1, np.array([[3.0, 0.1, 1.0]], np.float32),
+                                              categories=[4, 9, 11], total_inputs=12),
+                       InferenceConfig())
+    assert res.categories.tolist() == [4, 11]
+    assert res.final.data[0].tolist() == [5.0, 1.0]
+    # wrong-mode prepared structures raise ModelError (tests/test_parallel.py:246-252)
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=64, layers=2, connections_per_neuron=8, seed=1))
+    bad = engine.prepare_model(model, InferenceConfig(), "baseline")
+    with pytest.raises(ModelError):
+        engine.infer(model, ingest.generate_synthetic_inputs(64, 5, 0.5, seed=1),
+                     InferenceConfig(), mode="optimized", prepared=bad)
+
+
+def test_run_layer_step_and_counters(cuda_ok):
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=256, layers=1, connections_per_neuron=32, bias_value=-0.3, seed=5))
+    inputs = ingest.generate_synthetic_inputs(256, 100, 0.3, seed=6)
+    prep = engine.prepare_model(model, InferenceConfig(), "optimized")[0]
+    out = engine.run_layer_step(inputs, prep, model.bias, InferenceConfig(), "optimized")
+    ref = oracle.infer(model, inputs)
+    assert out.features.categories.tolist() == ref.categories.tolist()
+    assert out.weight_element_reads == prep.plan.total_slots * 2
+    assert out.feature_element_reads == prep.plan.num_fp * 100

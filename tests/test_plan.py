@@ -1,0 +1,127 @@
+"""Layout-builder tests (CPU only): the C++ plan is re-executed on the CPU in
+the kernel's exact order (tests/plan_emulator.py) and must match the oracle
+bit for bit -- generic +/- weights, uniform weights (scaled form), forced
+multi-stage blocks, every group size."""
+
+import numpy as np
+import pytest
+
+from conftest import random_layer
+from oracle import oracle
+from plan_emulator import emulate_layer
+from paper_2007_14152_b200 import engine, ingest
+from paper_2007_14152_b200.engine import PlanParams, build_plans
+from paper_2007_14152_b200.model import ModelError, make_layer_csr
+
+PARAMS = [
+    PlanParams(),
+    PlanParams(rows_per_group=1, reorder=False, allow_scaled=False),
+    PlanParams(rows_per_group=3),
+    PlanParams(rows_per_group=7, allow_scaled=False),
+    PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3),
+    PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2, max_groups=16),
+    PlanParams(rows_per_group=1, footprint_cap=1, record_cap=1, max_groups=1),
+]
+
+
+def _check(layer, params, rng, m=9):
+    n = layer.neurons
+    x = rng.uniform(0, 3, (n, m)).astype(np.float32)
+    bias = rng.uniform(-0.5, 0.5, n).astype(np.float32)
+    plan = build_plans([layer], params)[0]
+    got, act = emulate_layer(plan, bias, x)
+    ref, ref_act = oracle.layer(layer, bias, x)
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
+    assert np.array_equal(act, ref_act)
+    return plan
+
+
+@pytest.mark.parametrize("pi", range(len(PARAMS)))
+def test_plan_bit_exact_random_layers(pi):
+    rng = np.random.default_rng(100 + pi)
+    for _ in range(25):
+        n = int(rng.integers(1, 60))
+        layer = random_layer(rng, n, max_row_nnz=min(n, int(rng.integers(1, 12))))
+        _check(layer, PARAMS[pi], rng)
+
+
+@pytest.mark.parametrize("pi", range(len(PARAMS)))
+def test_plan_bit_exact_synthetic_layers(pi):
+    rng = np.random.default_rng(200 + pi)
+    for _ in range(6):
+        n = int(rng.integers(33, 300))
+        k = int(rng.integers(2, 33))
+        spec = ingest.GeneratorSpec(neurons=n, layers=2, connections_per_neuron=k,
+                                    seed=int(rng.integers(1 << 30)))
+        model = ingest.generate_synthetic_network(spec)
+        for layer in model.layers:
+            plan = _check(layer, PARAMS[pi], rng)
+            if PARAMS[pi].allow_scaled:
+                assert plan.scaled  # all weights 1/16: column-uniform
+
+
+def test_uniform_weight_random_layer_uses_scaled_form():
+    rng = np.random.default_rng(5)
+    layer = random_layer(rng, 40, 8, values=0.0625)
+    plan = _check(layer, PlanParams(rows_per_group=3), rng)
+    assert plan.scaled
+    layer2 = random_layer(rng, 40, 8)
+    plan2 = _check(layer2, PlanParams(rows_per_group=3), rng)
+    assert not plan2.scaled
+
+
+def test_dense_rows_force_multi_stage():
+    rng = np.random.default_rng(6)
+    n = 600
+    rows = np.repeat(np.arange(3), 500)
+    cols = np.concatenate([rng.choice(n, 500, replace=False) for _ in range(3)])
+    layer = make_layer_csr(n, rows, cols, rng.uniform(-1, 1, 1500).astype(np.float32))
+    plan = _check(layer, PlanParams(rows_per_group=3), rng, m=5)
+    stages = plan.stages.reshape(-1, 4)
+    assert len(stages) > plan.num_blocks  # some block has several stages
+    assert stages[:, 1].max() <= 192
+
+
+def test_sliding_window_layers_group_well():
+    """Generator layers are row-permuted sliding windows; the overlap ordering
+    must find them: ~K+R-1 union columns per group of R rows."""
+    model = ingest.generate_synthetic_network(
+        ingest.GeneratorSpec(neurons=4096, layers=3, connections_per_neuron=32, seed=1))
+    for plan in build_plans(model.layers, PlanParams()):
+        assert plan.rows_per_group == 7
+        per_group = plan.num_records / (4096 / 7)
+        assert per_group < 40.5, per_group
+        assert plan.num_fp / 4096 < 1.35
+
+
+def test_empty_and_degenerate_layers():
+    rng = np.random.default_rng(9)
+    empty = make_layer_csr(5, np.empty(0), np.empty(0), np.empty(0, np.float32))
+    for p in PARAMS:
+        _check(empty, p, rng)
+    single = make_layer_csr(1, np.array([0]), np.array([0]), np.array([2.0], np.float32))
+    for p in PARAMS:
+        _check(single, p, rng)
+
+
+def test_plan_rejects_bad_params():
+    layer = make_layer_csr(4, np.array([0]), np.array([1]), np.array([1.0], np.float32))
+    with pytest.raises(ModelError):
+        build_plans([layer], PlanParams(rows_per_group=5))
+    with pytest.raises(ModelError):
+        build_plans([layer], PlanParams(footprint_cap=0))
+
+
+def test_prepare_model_modes_and_stats():
+    model = ingest.generate_synthetic_network(
+        ingest.GeneratorSpec(neurons=256, layers=3, connections_per_neuron=16, seed=3))
+    cfg = engine.InferenceConfig()
+    opt = engine.prepare_model(model, cfg, "optimized")
+    base = engine.prepare_model(model, cfg, "baseline")
+    for p in base:
+        assert p.plan.rows_per_group == 1 and p.padding.overhead == 0.0
+    for p in opt:
+        assert p.plan.rows_per_group in (3, 7)
+        assert p.padding.padded_slots >= p.padding.nnz
+    with pytest.raises(ModelError):
+        engine.prepare_model(model, cfg, "fast")
