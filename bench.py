@@ -222,8 +222,10 @@ def run_ours(args, cfg):
         if world > 1:
             dist.barrier()
 
+    opts = engine.run_opts(net)
+
     def step(evs=None):
-        engine.stage_inputs(ws, x_dev, cats_dev)
+        engine.stage_inputs(ws, x_dev, cats_dev, net)
         if evs is None:
             return engine.run_layers(net, ws, m)
         ws.counts.zero_()
@@ -240,14 +242,18 @@ def run_ours(args, cfg):
                 engine._dptr(ws.y[o]), ws.ld, engine._dptr(ws.a[i]), engine._dptr(ws.cat[i]),
                 ctypes.c_void_p(ws.counts.data_ptr() + 4 * l), engine._dptr(ws.a[o]),
                 engine._dptr(ws.cat[o]), ctypes.c_void_p(ws.counts.data_ptr() + 4 * (l + 1)),
-                ctypes.byref(ws.scratch), ctypes.c_void_p(ws.work.data_ptr() + 4 * l), sp),
+                ctypes.byref(ws.scratch), ctypes.c_void_p(ws.work.data_ptr() + 4 * l),
+                ctypes.byref(opts), sp),
                 "spdnn_layer_forward")
         evs[L].record()
         return engine.DeviceRun(ws, L, m)
 
     # correctness of the timed configuration: categories after one step
-    step()
-    counts_chk, cats_chk, _ = engine.collect(engine.DeviceRun(ws, L, m), want_values=False)
+    run0 = step()
+    counts_chk, cats_chk, _ = engine.collect(run0, want_values=False)
+    assert run0.guard == 0, "FMA-form guard tripped on the bench workload"
+    log(f"[rank {rank}] arithmetic form: {'fma' if run0.fma else 'exact'}; "
+        f"survivors {int(counts_chk[-1])}")
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -327,7 +333,9 @@ def run_ours(args, cfg):
                        "survivors": int(counts[L]), "sum_active": int(counts[:L].sum()),
                        "l2": "inputs larger than L2 (Y = %.0f MB per buffer vs 126 MB)"
                              % (n * ws.ld * 4 / 1e6),
-                       "parallelism": f"batch-parallel x{world}" if world > 1 else "single"},
+                       "parallelism": f"batch-parallel x{world}" if world > 1 else "single",
+                       "arithmetic": "fma form (weights 2^-4, guard clean)" if opts.fma_form
+                                     else "exact form"},
             "e2e": {"value": edges_step / e2e_s / 1e12, "unit": "TE/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s * 1e3,

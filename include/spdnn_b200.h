@@ -60,8 +60,6 @@ typedef struct spdnn_plan_params {
   int32_t max_groups;       /* max row groups per block (<= warps per CTA) */
   int32_t record_cap;       /* max union records staged per block stage */
   int32_t reorder;          /* 1 = order rows by column overlap, 0 = identity */
-  int32_t allow_scaled;     /* 1 = use the column-scaled form when every input
-                               column carries one weight value */
 } spdnn_plan_params;
 
 typedef struct spdnn_plan spdnn_plan; /* opaque host plan for one layer */
@@ -81,7 +79,9 @@ typedef struct spdnn_plan_sizes_t {
   int64_t padded_slots;     /* num_records * R: multiply-add slots per feature */
   int32_t max_fp_per_stage;
   int32_t max_records_per_stage;
-  int32_t scaled;           /* 1: staging multiplies by fpw, records hold 0/1 */
+  int32_t pow2;             /* 1: every nonzero weight is +-2^e (FMA form allowed) */
+  int32_t wexp_min;         /* exponent range of the nonzero weights */
+  int32_t wexp_max;
 } spdnn_plan_sizes_t;
 
 /* Build the plan for one CSR layer (canonical CSR as in model.py:35-58).
@@ -104,16 +104,13 @@ int spdnn_plan_sizes(const spdnn_plan *plan, spdnn_plan_sizes_t *sizes);
  *   stages  int64[num_stages * 4]  {fp_offset, fp_count, rec_offset, rec_count}
  *   segs    int32[num_segs * 2]    {record offset relative to its stage, count}
  *   fp      int32[num_fp]          staged input neuron per smem slot
- *   fpw     float[num_fp]          its weight (scaled form) or 1.0
  *   rows    int32[num_groups * R]  output neuron per group row (-1 = padding)
  *   records uint32[num_records * record_words]
  *           word 0 = smem byte offset of the input neuron's tile row,
- *           words 1..R = fp32 weight bits per group row (0 = not connected);
- *           in the scaled form 1.0 / 0.0 connection masks
+ *           words 1..R = fp32 weight bits per group row (0 = not connected)
  */
 int spdnn_plan_export(const spdnn_plan *plan, int32_t *blocks, int64_t *stages,
-                      int32_t *segs, int32_t *fp, float *fpw, int32_t *rows,
-                      uint32_t *records);
+                      int32_t *segs, int32_t *fp, int32_t *rows, uint32_t *records);
 void spdnn_plan_free(spdnn_plan *plan);
 
 /* ---- device execution ---------------------------------------------------- */
@@ -124,7 +121,6 @@ typedef struct spdnn_layer_dev {
   const int64_t *stages;
   const int32_t *segs;
   const int32_t *fp;
-  const float *fpw;
   const int32_t *rows;
   const uint32_t *records;
   int64_t num_blocks;
@@ -132,7 +128,6 @@ typedef struct spdnn_layer_dev {
   int32_t record_words;
   int32_t max_fp_per_stage;
   int32_t max_records_per_stage;
-  int32_t scaled;
 } spdnn_layer_dev;
 
 /* Per-inference scratch shared by every layer launch (device pointers). */
@@ -140,7 +135,21 @@ typedef struct spdnn_scratch {
   int32_t *tile_done;      /* [ceil(M_cap/64)] zero-initialised */
   uint32_t *tile_alive;    /* [2*ceil(M_cap/64)] zero-initialised */
   int32_t *work;           /* [num_layers] zero-initialised work counters */
+  uint32_t *guard;         /* [1] zero-initialised; bit 0 = FMA-form guard
+                              tripped (rerun in the exact form), bit 1 =
+                              non-finite input (rerun with one row per group) */
 } spdnn_scratch;
+
+/* Arithmetic form of a launch (layer.cu):
+ *   fma_form = 0 : exact form, any weights: p = fl(y*w) then acc = fl(acc+p)
+ *   fma_form = 1 : acc = fma(y, w, acc); bit-identical when y*w is exact,
+ *                  i.e. all weights +-2^e and no input in (0, tiny) --
+ *                  tiny = 2^(-126 - min weight exponent); outputs below it
+ *                  set guard bit 0 (the next layer would not be exact). */
+typedef struct spdnn_run_opts {
+  int32_t fma_form;
+  float tiny;
+} spdnn_run_opts;
 
 /* One layer over the active features (engine.run_layer_step, engine.py:145-170):
  *   y_in   : float[N][ld]   neuron-major, the active feature j lives in column
@@ -156,7 +165,7 @@ int spdnn_layer_forward(const spdnn_layer_dev *layer, const float *bias,
                         const int32_t *a_in, const int64_t *cat_in,
                         const int32_t *m_in, int32_t *a_out, int64_t *cat_out,
                         int32_t *m_out, const spdnn_scratch *scratch,
-                        int32_t *work, void *stream);
+                        int32_t *work, const spdnn_run_opts *opts, void *stream);
 
 /* All layers back to back on `stream` (engine.infer's loop, engine.py:264-285).
  * Buffers ping-pong between index 0 and 1; counts[l] = active features
@@ -166,11 +175,14 @@ int spdnn_infer_layers(int64_t num_layers, const spdnn_layer_dev *layers,
                        const float *bias, float *y0, float *y1, int64_t ld,
                        int32_t *a0, int32_t *a1, int64_t *cat0, int64_t *cat1,
                        int32_t *counts, const spdnn_scratch *scratch,
-                       void *stream);
+                       const spdnn_run_opts *opts, void *stream);
 
-/* x: float[m][n] feature-major (FeatureBatch.data bytes) -> y: float[n][ld]. */
+/* x: float[m][n] feature-major (FeatureBatch.data bytes) -> y: float[n][ld].
+ * If guard != NULL: bit 0 |= some 0 < |x| < tiny or |x| > huge, bit 1 |= some
+ * x is NaN or inf. */
 int spdnn_transpose_in(const float *x, int64_t n, int64_t m, float *y,
-                       int64_t ld, void *stream);
+                       int64_t ld, uint32_t *guard, float tiny, float huge,
+                       void *stream);
 /* out[k][:] = y[:, a[perm[k]]] for k < m (feature-major result, i.e. the
  * (N, m) Fortran FeatureBatch layout). perm may be NULL (identity). */
 int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int32_t *a,

@@ -31,7 +31,7 @@ i32, i64 = ctypes.c_int32, ctypes.c_int64
 
 class PlanParams(ctypes.Structure):
     _fields_ = [("rows_per_group", i32), ("footprint_cap", i32), ("max_groups", i32),
-                ("record_cap", i32), ("reorder", i32), ("allow_scaled", i32)]
+                ("record_cap", i32), ("reorder", i32)]
 
 
 class PlanSizes(ctypes.Structure):
@@ -39,18 +39,23 @@ class PlanSizes(ctypes.Structure):
                 ("num_blocks", i64), ("num_stages", i64), ("num_groups", i64),
                 ("num_segs", i64), ("num_fp", i64), ("num_records", i64), ("nnz", i64),
                 ("padded_slots", i64), ("max_fp_per_stage", i32),
-                ("max_records_per_stage", i32), ("scaled", i32)]
+                ("max_records_per_stage", i32), ("pow2", i32), ("wexp_min", i32),
+                ("wexp_max", i32)]
 
 
 class LayerDev(ctypes.Structure):
-    _fields_ = [("blocks", P), ("stages", P), ("segs", P), ("fp", P), ("fpw", P),
+    _fields_ = [("blocks", P), ("stages", P), ("segs", P), ("fp", P),
                 ("rows", P), ("records", P), ("num_blocks", i64), ("rows_per_group", i32),
                 ("record_words", i32), ("max_fp_per_stage", i32),
-                ("max_records_per_stage", i32), ("scaled", i32)]
+                ("max_records_per_stage", i32)]
 
 
 class Scratch(ctypes.Structure):
-    _fields_ = [("tile_done", P), ("tile_alive", P), ("work", P)]
+    _fields_ = [("tile_done", P), ("tile_alive", P), ("work", P), ("guard", P)]
+
+
+class RunOpts(ctypes.Structure):
+    _fields_ = [("fma_form", i32), ("tiny", ctypes.c_float)]
 
 
 _lib = None
@@ -87,14 +92,16 @@ def lib():
         L.spdnn_plan_build.argtypes = [i64, P, P, P, ctypes.POINTER(PlanParams), ctypes.POINTER(P)]
         L.spdnn_plan_build_many.argtypes = [i64, i64, P, P, P, ctypes.POINTER(PlanParams), i32, P]
         L.spdnn_plan_sizes.argtypes = [P, ctypes.POINTER(PlanSizes)]
-        L.spdnn_plan_export.argtypes = [P, P, P, P, P, P, P, P]
+        L.spdnn_plan_export.argtypes = [P, P, P, P, P, P, P]
         L.spdnn_plan_free.argtypes = [P]
         L.spdnn_plan_free.restype = None
         L.spdnn_layer_forward.argtypes = [ctypes.POINTER(LayerDev), P, P, P, i64, P, P, P, P, P,
-                                          P, ctypes.POINTER(Scratch), P, P]
+                                          P, ctypes.POINTER(Scratch), P,
+                                          ctypes.POINTER(RunOpts), P]
         L.spdnn_infer_layers.argtypes = [i64, P, P, P, P, i64, P, P, P, P, P,
-                                         ctypes.POINTER(Scratch), P]
-        L.spdnn_transpose_in.argtypes = [P, i64, i64, P, i64, P]
+                                         ctypes.POINTER(Scratch), ctypes.POINTER(RunOpts), P]
+        L.spdnn_transpose_in.argtypes = [P, i64, i64, P, i64, P, ctypes.c_float,
+                                         ctypes.c_float, P]
         L.spdnn_gather_out.argtypes = [P, i64, i64, P, P, i64, P, P]
         L.spdnn_last_error.restype = ctypes.c_char_p
         L.spdnn_version.restype = ctypes.c_char_p

@@ -36,13 +36,13 @@ struct spdnn_plan {
   std::vector<int64_t> stages;   // 4 per stage
   std::vector<int32_t> segs;     // 2 per seg
   std::vector<int32_t> fp;
-  std::vector<float> fpw;        // per staged neuron: its (column-uniform) weight
   std::vector<int32_t> rows;
   std::vector<uint32_t> records;
   int64_t nnz = 0;
   int64_t num_groups = 0;
   int32_t max_fp = 0, max_rec = 0;
-  int32_t scaled = 0;            // 1: records hold 0/1 masks, staging scales by fpw
+  int32_t pow2 = 0;              // every nonzero weight is +-2^e (FMA form allowed)
+  int32_t wexp_min = 0, wexp_max = 0;
 };
 
 namespace {
@@ -118,21 +118,23 @@ std::vector<int32_t> overlap_order(int64_t n, const int64_t *rp, const int32_t *
   return order;
 }
 
-// True when every stored weight of each input column is the same value, so the
-// product y[c]*w[c] can be formed once per staged neuron instead of once per
-// (row, column). Bit-exact either way: the same fp32 product is added.
-bool column_uniform(int64_t n, const int64_t *rp, const int32_t *ci, const float *va,
-                    std::vector<float> &colw) {
-  colw.assign(n, 0.0f);
-  std::vector<uint8_t> seen(n, 0);
-  for (int64_t p = 0; p < rp[n]; p++) {
-    int32_t c = ci[p];
-    uint32_t a, b;
-    std::memcpy(&a, &va[p], 4);
-    if (!seen[c]) { seen[c] = 1; colw[c] = va[p]; continue; }
-    std::memcpy(&b, &colw[c], 4);
-    if (a != b) return false;
+// Exponent range when every nonzero weight is +-2^e with e in the normal
+// range: then y*w is exact for every normal product, which is what lets the
+// kernel use a single FFMA2 per (row, column) (layer.cu, "FMA form").
+bool pow2_weights(int64_t nnz, const float *va, int32_t &emin, int32_t &emax) {
+  emin = 1000;
+  emax = -1000;
+  for (int64_t p = 0; p < nnz; p++) {
+    uint32_t b;
+    std::memcpy(&b, &va[p], 4);
+    if ((b & 0x7fffffffu) == 0) continue;          // +-0: product is exactly 0
+    const uint32_t ex = (b >> 23) & 0xffu, man = b & 0x7fffffu;
+    if (man != 0 || ex == 0 || ex == 0xffu) return false;  // not a normal power of two
+    const int32_t e = (int32_t)ex - 127;
+    emin = std::min(emin, e);
+    emax = std::max(emax, e);
   }
+  if (emin > emax) { emin = 0; emax = 0; }  // no nonzero weights
   return true;
 }
 
@@ -179,8 +181,7 @@ int64_t total_records(const std::vector<Group> &gs) {
 double record_cost(int R) { return R == 1 ? 3.0 : (R == 3 ? 3.0 : 4.25); }
 
 void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
-          const std::vector<Group> &gs, const spdnn_plan_params &p,
-          const std::vector<float> *colw) {
+          const std::vector<Group> &gs, const spdnn_plan_params &p) {
   const int R = pl->R, RW = pl->RW;
   const int64_t n = pl->n;
   const int S = p.footprint_cap, RC = p.record_cap, GMAX = p.max_groups;
@@ -194,11 +195,7 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
     const int32_t *it = std::lower_bound(b, e, col);
     return (it != e && *it == col) ? va[it - ci] : 0.0f;
   };
-  auto connected = [&](int32_t row, int32_t col) -> bool {
-    const int32_t *b = ci + rp[row], *e = ci + rp[row + 1];
-    const int32_t *it = std::lower_bound(b, e, col);
-    return it != e && *it == col;
-  };
+
   pl->rows.resize(gs.size() * R);
   for (size_t g = 0; g < gs.size(); g++)
     for (int k = 0; k < R; k++) pl->rows[g * R + k] = gs[g].rows[k];
@@ -244,7 +241,6 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
       int64_t fp_off = (int64_t)pl->fp.size();
       for (int64_t i = c_lo; i < c_hi; i++) {
         pl->fp.push_back(fp_block[i]);
-        pl->fpw.push_back(colw ? (*colw)[fp_block[i]] : 1.0f);
         slot_of[fp_block[i]] = (int32_t)(i - c_lo);
       }
       int64_t rec_off = (int64_t)pl->records.size() / RW;
@@ -261,7 +257,6 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
           for (int k = 0; k < R; k++) {
             int32_t row = gs[gg].rows[k];
             float w = row >= 0 ? weight(row, c) : 0.0f;
-            if (colw) w = (row >= 0 && connected(row, c)) ? 1.0f : 0.0f;
             uint32_t bits;
             std::memcpy(&bits, &w, 4);
             pl->records[base + 1 + k] = bits;
@@ -331,10 +326,8 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
     pl->R = R;
     pl->RW = record_words(R);
     pl->num_groups = (int64_t)best.size();
-    std::vector<float> colw;
-    bool uni = p.allow_scaled && n > 0 && column_uniform(n, row_ptr, col_idx, values, colw);
-    pl->scaled = uni ? 1 : 0;
-    emit(pl, row_ptr, col_idx, values, best, p, uni ? &colw : nullptr);
+    pl->pow2 = pow2_weights(pl->nnz, values, pl->wexp_min, pl->wexp_max) ? 1 : 0;
+    emit(pl, row_ptr, col_idx, values, best, p);
   } catch (const std::bad_alloc &) {
     delete pl;
     return spdnn_fail(SPDNN_ENOMEM, "spdnn_plan_build: out of memory");
@@ -392,12 +385,14 @@ extern "C" int spdnn_plan_sizes(const spdnn_plan *pl, spdnn_plan_sizes_t *s) {
   s->padded_slots = s->num_records * pl->R;
   s->max_fp_per_stage = pl->max_fp;
   s->max_records_per_stage = pl->max_rec;
-  s->scaled = pl->scaled;
+  s->pow2 = pl->pow2;
+  s->wexp_min = pl->wexp_min;
+  s->wexp_max = pl->wexp_max;
   return SPDNN_OK;
 }
 
 extern "C" int spdnn_plan_export(const spdnn_plan *pl, int32_t *blocks, int64_t *stages,
-                                 int32_t *segs, int32_t *fp, float *fpw, int32_t *rows,
+                                 int32_t *segs, int32_t *fp, int32_t *rows,
                                  uint32_t *records) {
   if (!pl) return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_export: null plan");
   auto cp = [](auto *dst, const auto &v) {
@@ -407,7 +402,6 @@ extern "C" int spdnn_plan_export(const spdnn_plan *pl, int32_t *blocks, int64_t 
   cp(stages, pl->stages);
   cp(segs, pl->segs);
   cp(fp, pl->fp);
-  cp(fpw, pl->fpw);
   cp(rows, pl->rows);
   cp(records, pl->records);
   return SPDNN_OK;

@@ -77,10 +77,9 @@ class PlanParams:
     max_groups: int = 16         # row groups per block (one per warp)
     record_cap: int = 1024       # union records per block stage
     reorder: bool = True
-    allow_scaled: bool = True
 
 
-BASELINE_PARAMS = PlanParams(rows_per_group=1, reorder=False, allow_scaled=False)
+BASELINE_PARAMS = PlanParams(rows_per_group=1, reorder=False)
 OPTIMIZED_PARAMS = PlanParams()
 
 
@@ -99,7 +98,9 @@ class LayerPlan:
     neurons: int
     rows_per_group: int
     record_words: int
-    scaled: bool
+    pow2: bool             # every nonzero weight is +-2^e: the FMA form applies
+    wexp_min: int
+    wexp_max: int
     num_blocks: int
     max_fp_per_stage: int
     max_records_per_stage: int
@@ -109,7 +110,6 @@ class LayerPlan:
     stages: np.ndarray
     segs: np.ndarray
     fp: np.ndarray
-    fpw: np.ndarray
     rows: np.ndarray
     records: np.ndarray
 
@@ -129,7 +129,7 @@ class PreparedLayer:
 
 def _params_struct(p: PlanParams) -> _native.PlanParams:
     return _native.PlanParams(p.rows_per_group, p.footprint_cap, p.max_groups, p.record_cap,
-                              int(p.reorder), int(p.allow_scaled))
+                              int(p.reorder))
 
 
 def _export(handle) -> LayerPlan:
@@ -141,17 +141,17 @@ def _export(handle) -> LayerPlan:
         stages=np.zeros(s.num_stages * 4, np.int64),
         segs=np.zeros(s.num_segs * 2, np.int32),
         fp=np.zeros(s.num_fp, np.int32),
-        fpw=np.zeros(s.num_fp, np.float32),
         rows=np.zeros(s.num_groups * s.rows_per_group, np.int32),
         records=np.zeros(s.num_records * s.record_words, np.uint32),
     )
     ptr = lambda a: ctypes.c_void_p(a.ctypes.data)
     _native.check(L.spdnn_plan_export(handle, ptr(arrs["blocks"]), ptr(arrs["stages"]),
-                                      ptr(arrs["segs"]), ptr(arrs["fp"]), ptr(arrs["fpw"]),
+                                      ptr(arrs["segs"]), ptr(arrs["fp"]),
                                       ptr(arrs["rows"]), ptr(arrs["records"])),
                   "spdnn_plan_export")
     return LayerPlan(neurons=s.neurons, rows_per_group=s.rows_per_group,
-                     record_words=s.record_words, scaled=bool(s.scaled),
+                     record_words=s.record_words, pow2=bool(s.pow2),
+                     wexp_min=s.wexp_min, wexp_max=s.wexp_max,
                      num_blocks=s.num_blocks, max_fp_per_stage=s.max_fp_per_stage,
                      max_records_per_stage=s.max_records_per_stage,
                      num_records=s.num_records, num_fp=s.num_fp, **arrs)
@@ -247,15 +247,20 @@ class DeviceNetwork:
         self.neurons = int(bias.shape[0])
         self.modes = {p.mode for p in prepared}
         plans = [p.plan for p in prepared]
-        kinds = ("blocks", "stages", "segs", "fp", "fpw", "rows", "records")
+        kinds = ("blocks", "stages", "segs", "fp", "rows", "records")
         self.buffers = {}
         offsets = {k: [] for k in kinds}
         for k in kinds:
-            parts = [getattr(pl, k) for pl in plans]
+            parts = []
             off = 0
-            for a in parts:
+            for pl in plans:
+                a = getattr(pl, k)
+                pad = (-a.shape[0] * a.itemsize) % 32  # every layer's slice 32-byte aligned
+                parts.append(a)
+                if pad:
+                    parts.append(np.zeros(pad // a.itemsize, dtype=a.dtype))
                 offsets[k].append(off)
-                off += a.shape[0]
+                off += a.shape[0] + pad // a.itemsize
             cat = np.concatenate(parts) if parts else np.zeros(0, np.int32)
             if cat.dtype == np.uint32:
                 cat = cat.view(np.int32)
@@ -275,7 +280,16 @@ class DeviceNetwork:
             d.record_words = pl.record_words
             d.max_fp_per_stage = pl.max_fp_per_stage
             d.max_records_per_stage = pl.max_records_per_stage
-            d.scaled = int(pl.scaled)
+        # FMA form (one FFMA2 per (row, column)) is exact when every weight is
+        # +-2^e and no input falls below `tiny` (products stay normal) or above
+        # `huge` (no overflow); the kernels flag violations and infer() reruns
+        # in the exact form.
+        self.pow2 = bool(plans) and all(pl.pow2 for pl in plans)
+        emin = min((pl.wexp_min for pl in plans), default=0)
+        emax = max((pl.wexp_max for pl in plans), default=0)
+        self.tiny = float(np.ldexp(np.float32(1.0), -126 - emin)) if -126 - emin > -149 else 0.0
+        self.tiny = min(self.tiny, 1.0)
+        self.huge = float(np.ldexp(1.0, min(127, 126 - emax))) if emax < 126 else 0.0
         self.total_slots = [pl.total_slots for pl in plans]
         self.num_fp = [pl.num_fp for pl in plans]
         self.hbm_bytes = sum(int(b.numel() * b.element_size()) for b in self.buffers.values())
@@ -300,8 +314,9 @@ class Workspace:
         self.tile_done = torch.zeros(tiles, dtype=i32, device=device)
         self.tile_alive = torch.zeros(2 * tiles, dtype=i32, device=device)
         self.work = torch.zeros(max(1, num_layers), dtype=i32, device=device)
+        self.guard = torch.zeros(1, dtype=i32, device=device)
         self.scratch = _native.Scratch(self.tile_done.data_ptr(), self.tile_alive.data_ptr(),
-                                       self.work.data_ptr())
+                                       self.work.data_ptr(), self.guard.data_ptr())
         self.iota = torch.arange(self.ld, dtype=i32, device=device)
 
     def fits(self, neurons: int, m: int, num_layers: int) -> bool:
@@ -356,33 +371,58 @@ class DeviceRun:
         self.num_layers = num_layers
         self.m0 = m0
         self.out_index = num_layers % 2
+        self.fma = False
+        self.guard = 0  # filled by collect(): bit 0 FMA-form guard, bit 1 non-finite input
+
+    @property
+    def needs_exact_rerun(self) -> bool:
+        return bool(self.guard & 1) and self.fma
+
+    @property
+    def needs_unpadded_rerun(self) -> bool:
+        return bool(self.guard & 2)
 
 
-def stage_inputs(ws: Workspace, x_host_or_dev, categories, stream=None) -> None:
+def stage_inputs(ws: Workspace, x_host_or_dev, categories, net: "DeviceNetwork | None" = None
+                 ) -> None:
     """Copy (M, N) feature-major inputs into the workspace and lay them out
-    neuron-major (spdnn_transpose_in); A = 0..M-1; categories as given."""
+    neuron-major (spdnn_transpose_in, which also screens them for the FMA
+    form); A = 0..M-1; categories as given. Resets the guard flags."""
     torch = _torch()
     m = int(x_host_or_dev.shape[0])
     n = ws.neurons
+    ws.guard.zero_()
     if m:
         ws.x[:m].copy_(x_host_or_dev, non_blocking=True)
-        _native.check(_native.lib().spdnn_transpose_in(_dptr(ws.x), n, m, _dptr(ws.y[0]), ws.ld,
-                                                      _stream_ptr(torch)), "spdnn_transpose_in")
+        tiny = net.tiny if net is not None else 0.0
+        huge = net.huge if net is not None else 3.0e38
+        _native.check(_native.lib().spdnn_transpose_in(
+            _dptr(ws.x), n, m, _dptr(ws.y[0]), ws.ld, _dptr(ws.guard), tiny, huge,
+            _stream_ptr(torch)), "spdnn_transpose_in")
         ws.a[0][:m].copy_(ws.iota[:m])
         ws.cat[0][:m].copy_(categories, non_blocking=True)
 
 
-def run_layers(net: DeviceNetwork, ws: Workspace, m0: int) -> DeviceRun:
+def run_opts(net: DeviceNetwork, fma: bool | None = None) -> _native.RunOpts:
+    use = net.pow2 if fma is None else (fma and net.pow2)
+    return _native.RunOpts(int(use), net.tiny)
+
+
+def run_layers(net: DeviceNetwork, ws: Workspace, m0: int, fma: bool | None = None
+               ) -> DeviceRun:
     """Enqueue every layer on the current stream; no host synchronisation."""
     torch = _torch()
     ws.counts.zero_()
     ws.counts[0] = m0
     ws.work.zero_()
+    opts = run_opts(net, fma)
     _native.check(_native.lib().spdnn_infer_layers(
         net.num_layers, net.layer_devs, _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
         _dptr(ws.a[0]), _dptr(ws.a[1]), _dptr(ws.cat[0]), _dptr(ws.cat[1]), _dptr(ws.counts),
-        ctypes.byref(ws.scratch), _stream_ptr(torch)), "spdnn_infer_layers")
-    return DeviceRun(ws, net.num_layers, m0)
+        ctypes.byref(ws.scratch), ctypes.byref(opts), _stream_ptr(torch)), "spdnn_infer_layers")
+    run = DeviceRun(ws, net.num_layers, m0)
+    run.fma = bool(opts.fma_form)
+    return run
 
 
 def collect(run: DeviceRun, want_values: bool = True):
@@ -390,7 +430,8 @@ def collect(run: DeviceRun, want_values: bool = True):
     the per-layer active counts. One host synchronisation."""
     torch = _torch()
     ws = run.ws
-    counts = ws.counts[: run.num_layers + 1].cpu().numpy().astype(np.int64)
+    host = torch.cat([ws.counts[: run.num_layers + 1], ws.guard]).cpu().numpy().astype(np.int64)
+    counts, run.guard = host[:-1], int(host[-1])
     s = int(counts[run.num_layers]) if run.num_layers else run.m0
     o = run.out_index
     cats = ws.cat[o][:s]
@@ -464,16 +505,29 @@ def infer(model: NetworkModel, inputs: FeatureBatch, config: InferenceConfig,
     ws = workspace(n, m, model.num_layers)
     x = torch.from_numpy(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
     cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
-    stage_inputs(ws, x, cats)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    ev0.record()
-    run = run_layers(net, ws, m)
-    ev1.record()
-    torch.cuda.synchronize()
-    elapsed = time.perf_counter() - t0
-    counts, sorted_cats, vals = collect(run, want_values=values)
+    fma = None
+    elapsed = device = 0.0
+    for _attempt in range(3):
+        stage_inputs(ws, x, cats, net)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ev0.record()
+        run = run_layers(net, ws, m, fma)
+        ev1.record()
+        torch.cuda.synchronize()
+        elapsed += time.perf_counter() - t0
+        device += ev0.elapsed_time(ev1) / 1e3
+        counts, sorted_cats, vals = collect(run, want_values=values)
+        if run.needs_unpadded_rerun:
+            # NaN/inf inputs: zero-weight union slots would spread them to rows
+            # that never read them; one row per group has no such slots.
+            net = DeviceNetwork(_unpadded(prepared, model), model.bias)
+            fma = False
+        elif run.needs_exact_rerun:
+            fma = False
+        else:
+            break
     cats_np = sorted_cats.cpu().numpy().astype(np.int64)
     final = None
     if values:
@@ -482,7 +536,15 @@ def infer(model: NetworkModel, inputs: FeatureBatch, config: InferenceConfig,
     return InferenceResult(final=final, categories=cats_np.copy(),
                            per_layer=_outcomes(counts, net), elapsed_seconds=elapsed,
                            edges_processed=inputs.total_inputs * count_edges(model),
-                           device_seconds=ev0.elapsed_time(ev1) / 1e3)
+                           device_seconds=device)
+
+
+def _unpadded(prepared: Sequence[PreparedLayer], model: NetworkModel) -> list:
+    """Plans with one row per group (no zero-weight slots) for the same layers."""
+    if all(p.plan.rows_per_group == 1 for p in prepared):
+        return list(prepared)
+    plans = build_plans([p.csr for p in prepared], BASELINE_PARAMS)
+    return [replace(p, plan=pl) for p, pl in zip(prepared, plans)]
 
 
 # ---------------------------------------------------------------------------
@@ -496,14 +558,27 @@ def _one_layer(features: FeatureBatch, prepared: PreparedLayer, bias: np.ndarray
     net = DeviceNetwork([prepared], bias)
     ws = Workspace(n, m, 1, torch.device("cuda", torch.cuda.current_device()))
     x = torch.from_numpy(np.asarray(features.data).T)
-    stage_inputs(ws, x, torch.arange(m, dtype=torch.int64))
-    ws.counts.zero_()
-    ws.counts[0] = m
-    _native.check(_native.lib().spdnn_layer_forward(
-        ctypes.byref(net.layer_devs[0]), _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
-        _dptr(ws.a[0]), _dptr(ws.cat[0]), _dptr(ws.counts), _dptr(ws.a[1]), _dptr(ws.cat[1]),
-        ctypes.c_void_p(ws.counts.data_ptr() + 4), ctypes.byref(ws.scratch), _dptr(ws.work),
-        _stream_ptr(torch)), "spdnn_layer_forward")
+    fma = None
+    for _attempt in range(3):
+        stage_inputs(ws, x, torch.arange(m, dtype=torch.int64), net)
+        ws.counts.zero_()
+        ws.counts[0] = m
+        ws.work.zero_()
+        opts = run_opts(net, fma)
+        _native.check(_native.lib().spdnn_layer_forward(
+            ctypes.byref(net.layer_devs[0]), _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]),
+            ws.ld, _dptr(ws.a[0]), _dptr(ws.cat[0]), _dptr(ws.counts), _dptr(ws.a[1]),
+            _dptr(ws.cat[1]), ctypes.c_void_p(ws.counts.data_ptr() + 4), ctypes.byref(ws.scratch),
+            _dptr(ws.work), ctypes.byref(opts), _stream_ptr(torch)), "spdnn_layer_forward")
+        guard = int(ws.guard.item())
+        if guard & 2 and prepared.plan.rows_per_group != 1:
+            plan = build_plans([prepared.csr], BASELINE_PARAMS)[0]
+            net = DeviceNetwork([replace(prepared, plan=plan)], bias)
+            fma = False
+        elif guard & 1 and opts.fma_form:
+            fma = False
+        else:
+            break
     out = torch.empty((m, n), dtype=torch.float32, device=ws.y[1].device)
     _native.check(_native.lib().spdnn_gather_out(_dptr(ws.y[1]), n, ws.ld, _dptr(ws.iota),
                                                  ctypes.c_void_p(0), m, _dptr(out),

@@ -25,7 +25,6 @@ def emulate_layer(plan, bias, x):
         for s in range(ns):
             fp_off, fp_cnt, rec_off, rec_cnt = (int(v) for v in stages[s0 + s])
             cols = plan.fp[fp_off:fp_off + fp_cnt]
-            w_c = plan.fpw[fp_off:fp_off + fp_cnt]
             for gl in range(ng):
                 so, sc = (int(v) for v in segs[seg0 + s * ng + gl])
                 for r in rec[rec_off + so: rec_off + so + sc]:
@@ -33,15 +32,8 @@ def emulate_layer(plan, bias, x):
                     y = x[cols[slot]]
                     ws = r[1:1 + R].view(np.float32)
                     for k in range(R):
-                        if plan.scaled:
-                            p = (y * w_c[slot]).astype(np.float32)
-                            if ws[k] == 1.0:
-                                acc[gl, k] = acc[gl, k] + p
-                            else:
-                                assert ws[k] == 0.0
-                        else:
-                            p = (y * ws[k]).astype(np.float32)
-                            acc[gl, k] = acc[gl, k] + p
+                        p = (y * ws[k]).astype(np.float32)
+                        acc[gl, k] = acc[gl, k] + p
         for gl in range(ng):
             for k in range(R):
                 row = int(plan.rows[(g0 + gl) * R + k])

@@ -44,8 +44,8 @@ def _layer_case(layer, params, rng, m):
     assert np.array_equal(act, ref_act)
 
 
-PARAMS = [PlanParams(), PlanParams(rows_per_group=1, reorder=False, allow_scaled=False),
-          PlanParams(rows_per_group=3), PlanParams(rows_per_group=7, allow_scaled=False),
+PARAMS = [PlanParams(), PlanParams(rows_per_group=1, reorder=False),
+          PlanParams(rows_per_group=3), PlanParams(rows_per_group=7, reorder=False),
           PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3),
           PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2)]
 
@@ -201,3 +201,62 @@ def test_run_layer_step_and_counters(cuda_ok):
     assert out.features.categories.tolist() == ref.categories.tolist()
     assert out.weight_element_reads == prep.plan.total_slots * 2
     assert out.feature_element_reads == prep.plan.num_fp * 100
+
+
+def _pow2_layer(rng, n, k):
+    from paper_2007_14152_b200.model import make_layer_csr
+    rows = np.repeat(np.arange(n), k)
+    cols = np.concatenate([rng.choice(n, k, replace=False) for _ in range(n)])
+    vals = (rng.choice([-1.0, 1.0], n * k) * 2.0 ** rng.integers(-6, 3, n * k)).astype(np.float32)
+    return make_layer_csr(n, rows, cols, vals)
+
+
+def test_fma_form_power_of_two_weights(cuda_ok):
+    """+-2^e weights take the one-FFMA2 path; results stay bit-identical."""
+    rng = np.random.default_rng(44)
+    n = 200
+    layers = [_pow2_layer(rng, n, 12) for _ in range(4)]
+    model = NetworkModel(neurons=n, layers=layers, bias=np.full(n, -0.05, np.float32))
+    prep = engine.prepare_model(model, InferenceConfig(), "optimized")
+    assert all(p.plan.pow2 for p in prep)
+    inputs = make_feature_batch(n, rng.uniform(0, 1, (n, 150)).astype(np.float32))
+    ref = oracle.infer(model, inputs)
+    res = engine.infer(model, inputs, InferenceConfig(), prepared=prep)
+    assert np.array_equal(res.categories, ref.categories)
+    assert same_bits(res.final.data, ref.final)
+
+
+def test_fma_guard_tiny_inputs_rerun_exact(cuda_ok):
+    """Inputs whose products with 2^-4 would be subnormal trip the guard and
+    the engine reruns in the exact form: still bit-identical."""
+    n = 64
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=n, layers=2, connections_per_neuron=16, bias_value=0.0, seed=3))
+    rng = np.random.default_rng(3)
+    x = rng.uniform(0, 1, (n, 70)).astype(np.float32)
+    x[::3, ::2] = np.float32(3e-38) * rng.uniform(0.1, 1, x[::3, ::2].shape).astype(np.float32)
+    inputs = make_feature_batch(n, x)
+    ref = oracle.infer(model, inputs)
+    res = engine.infer(model, inputs, InferenceConfig())
+    assert np.array_equal(res.categories, ref.categories)
+    assert same_bits(res.final.data, ref.final)
+
+
+def test_nonfinite_inputs_rerun_unpadded(cuda_ok):
+    """NaN / inf inputs: zero-weight union slots would spread them; the engine
+    reruns with one row per group and matches the reference semantics."""
+    n = 96
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=n, layers=3, connections_per_neuron=8, bias_value=-0.1, seed=9))
+    rng = np.random.default_rng(9)
+    x = rng.uniform(0, 1, (n, 40)).astype(np.float32)
+    x[5, 3] = np.nan
+    x[17, 9] = np.inf
+    inputs = make_feature_batch(n, x)
+    ref = oracle.infer(model, inputs)
+    res = engine.infer(model, inputs, InferenceConfig())
+    assert np.array_equal(res.categories, ref.categories)
+    a, b = np.asarray(res.final.data), np.asarray(ref.final)
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    ok = ~np.isnan(a)
+    assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))

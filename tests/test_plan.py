@@ -1,6 +1,6 @@
 """Layout-builder tests (CPU only): the C++ plan is re-executed on the CPU in
 the kernel's exact order (tests/plan_emulator.py) and must match the oracle
-bit for bit -- generic +/- weights, uniform weights (scaled form), forced
+bit for bit -- generic +/- weights, power-of-two weights, forced
 multi-stage blocks, every group size."""
 
 import numpy as np
@@ -15,9 +15,9 @@ from paper_2007_14152_b200.model import ModelError, make_layer_csr
 
 PARAMS = [
     PlanParams(),
-    PlanParams(rows_per_group=1, reorder=False, allow_scaled=False),
+    PlanParams(rows_per_group=1, reorder=False),
     PlanParams(rows_per_group=3),
-    PlanParams(rows_per_group=7, allow_scaled=False),
+    PlanParams(rows_per_group=7, reorder=False),
     PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3),
     PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2, max_groups=16),
     PlanParams(rows_per_group=1, footprint_cap=1, record_cap=1, max_groups=1),
@@ -56,18 +56,22 @@ def test_plan_bit_exact_synthetic_layers(pi):
         model = ingest.generate_synthetic_network(spec)
         for layer in model.layers:
             plan = _check(layer, PARAMS[pi], rng)
-            if PARAMS[pi].allow_scaled:
-                assert plan.scaled  # all weights 1/16: column-uniform
+            assert plan.pow2 and plan.wexp_min == plan.wexp_max == -4  # all weights 1/16
 
 
-def test_uniform_weight_random_layer_uses_scaled_form():
+def test_power_of_two_detection():
     rng = np.random.default_rng(5)
     layer = random_layer(rng, 40, 8, values=0.0625)
     plan = _check(layer, PlanParams(rows_per_group=3), rng)
-    assert plan.scaled
+    assert plan.pow2 and plan.wexp_min == -4
     layer2 = random_layer(rng, 40, 8)
     plan2 = _check(layer2, PlanParams(rows_per_group=3), rng)
-    assert not plan2.scaled
+    assert not plan2.pow2
+    vals = np.array([0.5, -2.0, 0.0, 8.0], np.float32)
+    from paper_2007_14152_b200.model import make_layer_csr
+    l3 = make_layer_csr(4, np.array([0, 1, 2, 3]), np.array([1, 2, 3, 0]), vals)
+    p3 = build_plans([l3], PlanParams())[0]
+    assert p3.pow2 and (p3.wexp_min, p3.wexp_max) == (-1, 3)
 
 
 def test_dense_rows_force_multi_stage():

@@ -25,7 +25,7 @@ ws = engine.workspace(model.neurons, m, model.num_layers)
 x = torch.from_numpy(np.ascontiguousarray(np.asarray(inputs.data).T)).cuda()
 c = torch.from_numpy(np.ascontiguousarray(inputs.categories)).cuda()
 for _ in range(steps):
-    engine.stage_inputs(ws, x, c)
+    engine.stage_inputs(ws, x, c, net)
     run = engine.run_layers(net, ws, m)
 torch.cuda.synchronize()
 counts, cats, _ = engine.collect(run, want_values=False)
