@@ -48,9 +48,11 @@ enum {
   SPDNN_ERANGE = 4    /* index exceeds the layout's range */
 };
 
-/* Feature-tile width: every layer launch processes features in tiles of 64
- * (32 lanes x 2 fp32 features). */
-#define SPDNN_TILE_FEATURES 64
+/* Feature-tile width: every work item covers 128 active features
+ * (32 lanes x 4 fp32 features, two f32x2 register pairs per lane). One staged
+ * input neuron is therefore a 512-byte shared-memory row. */
+#define SPDNN_TILE_FEATURES 128
+#define SPDNN_STAGED_ROW_BYTES 512
 
 /* ---- one-time layout conversion (host, C++) ----------------------------- */
 
@@ -70,15 +72,16 @@ typedef struct spdnn_plan_sizes_t {
   int32_t rows_per_group;   /* R actually used */
   int32_t record_words;     /* 32-bit words per union record (2, 4 or 8) */
   int64_t num_blocks;
-  int64_t num_stages;
+  int64_t num_extra_stages; /* stages beyond the first of multi-stage blocks */
   int64_t num_groups;
-  int64_t num_segs;
-  int64_t num_fp;           /* staged input neurons, summed over stages */
+  int64_t num_meta;         /* int32 words of per-block metadata */
   int64_t num_records;      /* union records (one per (group, input neuron)) */
+  int64_t num_fp;           /* staged input neurons, summed over all stages */
   int64_t nnz;
   int64_t padded_slots;     /* num_records * R: multiply-add slots per feature */
   int32_t max_fp_per_stage;
   int32_t max_records_per_stage;
+  int32_t max_meta_per_block;
   int32_t pow2;             /* 1: every nonzero weight is +-2^e (FMA form allowed) */
   int32_t wexp_min;         /* exponent range of the nonzero weights */
   int32_t wexp_max;
@@ -98,19 +101,22 @@ int spdnn_plan_build_many(int64_t num_layers, int64_t n,
                           spdnn_plan **out);
 int spdnn_plan_sizes(const spdnn_plan *plan, spdnn_plan_sizes_t *sizes);
 /* Copy the plan into caller-owned host buffers sized from spdnn_plan_sizes:
- *   blocks  int32[num_blocks * 8]  {first_group, num_groups, first_stage,
- *                                   num_stages, first_seg_lo, first_seg_hi,
- *                                   0, 0}
- *   stages  int64[num_stages * 4]  {fp_offset, fp_count, rec_offset, rec_count}
- *   segs    int32[num_segs * 2]    {record offset relative to its stage, count}
- *   fp      int32[num_fp]          staged input neuron per smem slot
- *   rows    int32[num_groups * R]  output neuron per group row (-1 = padding)
+ *   blocks  int32[num_blocks * 8]  {g_first, ng, nst, first_extra_stage,
+ *                                   meta_off, fp_cnt, rec_off, rec_cnt}
+ *                                   (meta/records of the block's first stage)
+ *   stages  int32[num_extra_stages * 4] {meta_off, fp_cnt, rec_off, rec_cnt}
+ *           (a block with nst > 1 holds exactly one group)
+ *   meta    int32[num_meta]: per block, 16-byte aligned:
+ *           fp_cnt input neurons (smem slot order), pad to 4,
+ *           ng x {record offset relative to rec_off, record count},
+ *           ng x R output neurons (-1 = padding row), pad to 4
  *   records uint32[num_records * record_words]
- *           word 0 = smem byte offset of the input neuron's tile row,
- *           words 1..R = fp32 weight bits per group row (0 = not connected)
+ *           word 0 = smem byte offset of the input neuron's staged row
+ *           (slot * SPDNN_STAGED_ROW_BYTES), words 1..R = fp32 weight bits
+ *           per group row (0 = not connected); per group ascending neuron
  */
-int spdnn_plan_export(const spdnn_plan *plan, int32_t *blocks, int64_t *stages,
-                      int32_t *segs, int32_t *fp, int32_t *rows, uint32_t *records);
+int spdnn_plan_export(const spdnn_plan *plan, int32_t *blocks, int32_t *stages,
+                      int32_t *meta, uint32_t *records);
 void spdnn_plan_free(spdnn_plan *plan);
 
 /* ---- device execution ---------------------------------------------------- */
@@ -118,22 +124,22 @@ void spdnn_plan_free(spdnn_plan *plan);
 /* Device-resident plan of one layer (pointers into device memory). */
 typedef struct spdnn_layer_dev {
   const int32_t *blocks;
-  const int64_t *stages;
-  const int32_t *segs;
-  const int32_t *fp;
-  const int32_t *rows;
+  const int32_t *stages;
+  const int32_t *meta;
   const uint32_t *records;
   int64_t num_blocks;
   int32_t rows_per_group;
   int32_t record_words;
   int32_t max_fp_per_stage;
   int32_t max_records_per_stage;
+  int32_t max_meta_per_block;
+  int32_t pad_;
 } spdnn_layer_dev;
 
 /* Per-inference scratch shared by every layer launch (device pointers). */
 typedef struct spdnn_scratch {
-  int32_t *tile_done;      /* [ceil(M_cap/64)] zero-initialised */
-  uint32_t *tile_alive;    /* [2*ceil(M_cap/64)] zero-initialised */
+  int32_t *tile_done;      /* [ceil(M_cap/128)] zero-initialised */
+  uint32_t *tile_alive;    /* [4*ceil(M_cap/128)] zero-initialised */
   int32_t *work;           /* [num_layers] zero-initialised work counters */
   uint32_t *guard;         /* [1] zero-initialised; bit 0 = FMA-form guard
                               tripped (rerun in the exact form), bit 1 =

@@ -36,18 +36,18 @@ class PlanParams(ctypes.Structure):
 
 class PlanSizes(ctypes.Structure):
     _fields_ = [("neurons", i64), ("rows_per_group", i32), ("record_words", i32),
-                ("num_blocks", i64), ("num_stages", i64), ("num_groups", i64),
-                ("num_segs", i64), ("num_fp", i64), ("num_records", i64), ("nnz", i64),
+                ("num_blocks", i64), ("num_extra_stages", i64), ("num_groups", i64),
+                ("num_meta", i64), ("num_records", i64), ("num_fp", i64), ("nnz", i64),
                 ("padded_slots", i64), ("max_fp_per_stage", i32),
-                ("max_records_per_stage", i32), ("pow2", i32), ("wexp_min", i32),
-                ("wexp_max", i32)]
+                ("max_records_per_stage", i32), ("max_meta_per_block", i32), ("pow2", i32),
+                ("wexp_min", i32), ("wexp_max", i32)]
 
 
 class LayerDev(ctypes.Structure):
-    _fields_ = [("blocks", P), ("stages", P), ("segs", P), ("fp", P),
-                ("rows", P), ("records", P), ("num_blocks", i64), ("rows_per_group", i32),
-                ("record_words", i32), ("max_fp_per_stage", i32),
-                ("max_records_per_stage", i32)]
+    _fields_ = [("blocks", P), ("stages", P), ("meta", P), ("records", P),
+                ("num_blocks", i64), ("rows_per_group", i32), ("record_words", i32),
+                ("max_fp_per_stage", i32), ("max_records_per_stage", i32),
+                ("max_meta_per_block", i32), ("pad_", i32)]
 
 
 class Scratch(ctypes.Structure):
@@ -92,7 +92,7 @@ def lib():
         L.spdnn_plan_build.argtypes = [i64, P, P, P, ctypes.POINTER(PlanParams), ctypes.POINTER(P)]
         L.spdnn_plan_build_many.argtypes = [i64, i64, P, P, P, ctypes.POINTER(PlanParams), i32, P]
         L.spdnn_plan_sizes.argtypes = [P, ctypes.POINTER(PlanSizes)]
-        L.spdnn_plan_export.argtypes = [P, P, P, P, P, P, P]
+        L.spdnn_plan_export.argtypes = [P, P, P, P, P]
         L.spdnn_plan_free.argtypes = [P]
         L.spdnn_plan_free.restype = None
         L.spdnn_layer_forward.argtypes = [ctypes.POINTER(LayerDev), P, P, P, i64, P, P, P, P, P,

@@ -8,33 +8,32 @@
 //   engine.compact_active       engine.py:130-142  (keep alive features)
 //   engine.infer layer loop     engine.py:264-285
 //
-// Work item = (row block b of the layer plan, tile t of 64 active features).
-// Persistent CTAs pull items from a per-layer atomic counter and run a
-// two-deep pipeline: while item k is computed out of smem buffer k&1, the
-// cp.async copies of item k+1 (its staged input neurons and its union
-// records) land in buffer (k+1)&1.
-//
-// Per item:
-//   1. staging (cp.async): for every input neuron c of the block footprint,
-//      the 64 features' values y_in[c][a_in[64t + f]] -> one 256-byte smem
-//      row (y_in is neuron-major and a_in mostly contiguous, so the global
-//      reads are 128-byte coalesced segments); plus the block's records;
-//   2. each warp takes one row group (R rows) at a time; lane l holds
-//      features (64t + l, 64t + l + 32) as one f32x2 register pair. Per union
-//      record (one input neuron, ascending neuron index) one LDS.64 fetches
-//      the pair and each row k accumulates it with weight w_k (0 where row k
-//      does not connect). Every row therefore adds its own products in
-//      ascending column order, interleaved with exact +0 terms: bit-equal to
-//      the reference's CSR sum (kernels.py:27-37, separate mul and add).
-//        FMA form  (all weights +-2^e): acc = fma(y, w, acc). The product is
-//                  exact, so fma == fl(acc + fl(y*w)). A value small enough
-//                  for y*w to underflow trips a guard flag and the engine
-//                  reruns with the exact form (never seen on real data).
-//        exact form (any weights): p = fma(y, w, -0) == fl(y*w), acc += p;
-//   3. epilogue: v = fl(acc + bias), comparison clamp (NaN kept,
-//      kernels.py:33-36), store y_out[row][64t + f], alive |= v > 0;
-//   4. the CTA finishing the last row block of tile t appends the tile's
-//      alive features to a_out / cat_out (pruning without a pass over Y).
+// Work item = (tile t of 128 active features, row block b of the layer plan).
+// One persistent CTA per SM, warp-specialised:
+//   * 1 producer warp pulls items from a per-layer atomic counter and fills a
+//     ring of shared-memory buffers with cp.async: the block's metadata and
+//     union records (contiguous 16-byte chunks) and, for every staged input
+//     neuron c of the block footprint, the tile's 128 feature values
+//     y_in[c][a_in[128t + f]] (one 16-byte copy per lane when the lane's four
+//     features are contiguous, else four 4-byte gathers). Completion is
+//     tracked by an mbarrier per buffer (cp.async.mbarrier.arrive.noinc);
+//   * 16 consumer warps each own one row group (R output rows) of the item.
+//     Lane l holds features 4l..4l+3 of the tile as two f32x2 register pairs.
+//     Per union record (one input neuron, ascending neuron index): one
+//     LDS.128 of the four values, and per row k two FFMA2 with weight w_k
+//     (0 where row k does not connect). Every row adds its own products in
+//     ascending column order, interleaved with exact +0 terms: bit-equal to
+//     the reference's CSR sum (kernels.py:27-37, separate mul and add):
+//        FMA form  (all weights +-2^e): acc = fma(y, w, acc); y*w is exact,
+//                  so fma == fl(acc + fl(y*w)). Outputs small enough that the
+//                  next layer's products could underflow set a guard bit and
+//                  the engine reruns in the exact form.
+//        exact form (any weights): p = fma(y, w, -0) == fl(y*w); acc += p.
+//     Epilogue: v = fl(acc + bias), comparison clamp (NaN kept,
+//     kernels.py:33-36), 16-byte store of the four features, alive |= v > 0;
+//   * the last consumer warp to finish an item publishes its activity bits;
+//     the item that completes tile t appends the tile's alive features to
+//     a_out / cat_out (pruning without a pass over Y).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,9 +43,12 @@
 
 namespace {
 
-constexpr int kTile = 64;
-constexpr int kWarps = 16;
-constexpr int kThreads = kWarps * 32;
+constexpr int kTile = SPDNN_TILE_FEATURES;  // 128
+constexpr int kRowBytes = SPDNN_STAGED_ROW_BYTES;
+constexpr int kConsumerWarps = 16;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kBufs = 2;
+constexpr int kHeaderBytes = 64;
 
 typedef unsigned long long u64;
 
@@ -77,20 +79,39 @@ __device__ __forceinline__ float clamp32(float v) {
   return v;
 }
 
+// ---- async copy + mbarrier primitives -------------------------------------
+
 __device__ __forceinline__ void cp_async4(uint32_t saddr, const void *gmem, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(saddr), "l"(gmem),
                "r"(valid ? 4 : 0));
 }
-__device__ __forceinline__ void cp_async8(uint32_t saddr, const void *gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
-}
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar)
+               : "memory");
+}
+// arrives on `bar` when all prior cp.async of this thread have landed
+__device__ __forceinline__ void mbar_cp_async_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 
 struct LayerArgs {
@@ -108,11 +129,22 @@ struct LayerArgs {
   int32_t *tile_done;
   uint32_t *tile_alive;
   int32_t *work;
-  uint32_t *guard;     // bit 0: an output in (0, tiny) was produced
-  float tiny;          // FMA form is exact for next-layer inputs >= tiny
+  uint32_t *guard;     // bit 0: an output in (0, tiny) was produced (FMA form)
+  float tiny;
   float negz;          // -0.0f, opaque to the compiler (exact form)
-  uint32_t buf_bytes;  // bytes of one pipeline buffer (ysm + rsm)
-  uint32_t ysm_bytes;
+  uint32_t buf_bytes;  // one ring buffer: header | meta | records | y rows
+  uint32_t meta_bytes;
+  uint32_t rec_bytes;
+};
+
+// Ring-buffer header written by the producer (one per buffer fill).
+struct Header {
+  int item;     // -1: no more work
+  int t, b;
+  int stage, nst;
+  int ng;
+  int rec_cnt;  // records of this stage (multi-stage: all belong to group 0)
+  int fp_cnt;
 };
 
 template <int R>
@@ -154,223 +186,304 @@ struct Rec<7> {
   }
 };
 
-// Accumulate one segment of union records into acc[0..R).
+// acc[2k], acc[2k+1]: row k, features (4l, 4l+1) and (4l+2, 4l+3).
 template <int R, bool FMA>
 __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int cnt,
-                                           const char *ysm, int lane, u64 negz2) {
-  const char *ybase = ysm + lane * 8;
+                                           const char *ybase, u64 negz2) {
 #pragma unroll 2
   for (int i = 0; i < cnt; i++) {
     uint32_t off;
     float w[R];
     Rec<R>::load(recs + i * Rec<R>::W, off, w);
-    const u64 y = *reinterpret_cast<const u64 *>(ybase + off);
+    const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ybase + off);
 #pragma unroll
     for (int k = 0; k < R; k++) {
-      if (FMA) acc[k] = fma2(y, w[k], acc[k]);
-      else acc[k] = add2(acc[k], fma2(y, w[k], negz2));
+      if (FMA) {
+        acc[2 * k] = fma2(y.x, w[k], acc[2 * k]);
+        acc[2 * k + 1] = fma2(y.y, w[k], acc[2 * k + 1]);
+      } else {
+        acc[2 * k] = add2(acc[2 * k], fma2(y.x, w[k], negz2));
+        acc[2 * k + 1] = add2(acc[2 * k + 1], fma2(y.y, w[k], negz2));
+      }
     }
   }
 }
 
 // Bias, clamp, store, activity (+ FMA-form guard) for one finished group.
 template <int R, bool FMA>
-__device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, int g, int t,
-                                         int lane, bool v0, bool v1, uint32_t *s_alive) {
-  bool al0 = false, al1 = false, tiny = false;
-  const int j0 = t * kTile + lane;
+__device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, const int *rows,
+                                         int t, int lane, int M, uint32_t *s_alive) {
+  const int j0 = t * kTile + 4 * lane;
+  bool alive[4] = {false, false, false, false};
+  bool tiny = false;
+  const bool full = j0 + 3 < M;
 #pragma unroll
   for (int k = 0; k < R; k++) {
-    const int row = __ldg(A.L.rows + (int64_t)g * R + k);
+    const int row = rows[k];
     if (row < 0) continue;
     const float b = __ldg(A.bias + row);
-    float x0, x1;
-    unpack2(acc[k], x0, x1);
-    x0 = clamp32(__fadd_rn(x0, b));
-    x1 = clamp32(__fadd_rn(x1, b));
+    float x[4];
+    unpack2(acc[2 * k], x[0], x[1]);
+    unpack2(acc[2 * k + 1], x[2], x[3]);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      x[q] = clamp32(__fadd_rn(x[q], b));
+      alive[q] |= (x[q] > 0.0f);
+      if (FMA) tiny |= (x[q] > 0.0f && x[q] < A.tiny && j0 + q < M);
+    }
     float *dst = A.y_out + (int64_t)row * A.ld + j0;
-    if (v0) dst[0] = x0;
-    if (v1) dst[32] = x1;
-    al0 |= (x0 > 0.0f);
-    al1 |= (x1 > 0.0f);
-    if (FMA) tiny |= (v0 && x0 > 0.0f && x0 < A.tiny) || (v1 && x1 > 0.0f && x1 < A.tiny);
+    if (full) {
+      *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+        if (j0 + q < M) dst[q] = x[q];
+    }
   }
-  const unsigned m0 = __ballot_sync(0xffffffffu, al0 && v0);
-  const unsigned m1 = __ballot_sync(0xffffffffu, al1 && v1);
-  if (lane == 0) {
-    if (m0) atomicOr(&s_alive[0], m0);
-    if (m1) atomicOr(&s_alive[1], m1);
+  // word w of the 128-bit tile mask holds features 32w..32w+31 (lanes 8w..8w+7)
+  uint32_t mine = 0;
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+    if (alive[q] && j0 + q < M) mine |= 1u << q;
+  mine <<= 4 * (lane & 7);
+#pragma unroll
+  for (int w = 0; w < 4; w++) {
+    const uint32_t word = __reduce_or_sync(0xffffffffu, (lane >> 3) == w ? mine : 0u);
+    if (lane == 0 && word) atomicOr(&s_alive[w], word);
   }
   if (FMA && tiny) atomicOr(A.guard, 1u);
 }
 
-struct Item {
-  int t, b, ng, g_first, s_first, nst;
-  int64_t seg0;
-};
-
-__device__ __forceinline__ Item decode(const LayerArgs &A, int item, int nb) {
-  Item it;
-  it.t = item / nb;
-  it.b = item - it.t * nb;
-  const int4 q = __ldg(reinterpret_cast<const int4 *>(A.L.blocks + (int64_t)it.b * 8));
-  const int2 s = __ldg(reinterpret_cast<const int2 *>(A.L.blocks + (int64_t)it.b * 8 + 4));
-  it.g_first = q.x;
-  it.ng = q.y;
-  it.s_first = q.z;
-  it.nst = q.w;
-  it.seg0 = (int64_t)(uint32_t)s.x | ((int64_t)s.y << 32);
-  return it;
-}
-
-// Issue the cp.async copies of one stage of an item into buffer `sbuf`
-// (shared-window address). Threads own fixed lanes (tid % 32).
-template <int RW>
-__device__ __forceinline__ void issue_stage(const LayerArgs &A, const Item &it, int s,
-                                            uint32_t sbuf, int tid, int M) {
-  const int lane = tid & 31;
-  const int j0 = it.t * kTile + lane, j1 = j0 + 32;
-  const bool v0 = j0 < M, v1 = j1 < M;
-  const int c0 = v0 ? __ldg(A.a_in + j0) : 0;
-  const int c1 = v1 ? __ldg(A.a_in + j1) : 0;
-  const int64_t *st = A.L.stages + (int64_t)(it.s_first + s) * 4;
-  const int64_t fp_off = __ldg(st + 0), rec_off = __ldg(st + 2);
-  const int fp_cnt = (int)__ldg(st + 1), rec_cnt = (int)__ldg(st + 3);
-  const uint32_t ydst = sbuf + lane * 8;
-  for (int slot = tid >> 5; slot < fp_cnt; slot += kWarps) {
-    const int64_t c = __ldg(A.L.fp + fp_off + slot);
-    const float *src = A.y_in + c * A.ld;
-    cp_async4(ydst + slot * 256, src + c0, v0);
-    cp_async4(ydst + slot * 256 + 4, src + c1, v1);
-  }
-  const uint32_t rdst = sbuf + A.ysm_bytes;
-  const uint32_t *rg = A.L.records + rec_off * RW;
-  if (RW >= 4) {
-    const int chunks = rec_cnt * RW / 4;
-    for (int i = tid; i < chunks; i += kThreads) cp_async16(rdst + 16 * i, rg + 4 * i);
+// Contiguous words -> smem: 16-byte chunks when the source is 16-byte
+// aligned (ALIGN_WORDS = 4: meta, R = 3 / 7 records), else 8-byte chunks.
+template <int ALIGN_WORDS>
+__device__ __forceinline__ void copy_words(uint32_t sdst, const uint32_t *src, int words,
+                                           int lane) {
+  if (ALIGN_WORDS >= 4) {
+    for (int i = lane; i < (words >> 2); i += 32) cp_async16(sdst + 16 * i, src + 4 * i);
   } else {
-    const int chunks = rec_cnt * RW / 2;
-    for (int i = tid; i < chunks; i += kThreads) cp_async8(rdst + 8 * i, rg + 2 * i);
+    for (int i = lane; i < (words >> 1); i += 32) cp_async8(sdst + 8 * i, src + 2 * i);
   }
 }
 
 template <int R, bool FMA>
-__global__ void __launch_bounds__(kThreads) layer_kernel(LayerArgs A) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ int s_next;
-  __shared__ uint32_t s_alive[2][2];
+__global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
+  extern __shared__ __align__(128) char smem[];
+  __shared__ __align__(8) u64 s_full[kBufs], s_empty[kBufs];
+  __shared__ uint32_t s_alive[kBufs][4];
+  __shared__ int s_done[kBufs];
 
   constexpr int RW = Rec<R>::W;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *A.m_in;
   if (M <= 0) return;
   const int nb = (int)A.L.num_blocks;
   const int tiles = (M + kTile - 1) / kTile;
   const int items = tiles * nb;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
-  const u64 negz2 = pack2(A.negz, A.negz);
+  const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
+  const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(&s_empty[0]);
 
-  if (tid == 0) s_next = atomicAdd(A.work, 1);
-  if (tid < 4) s_alive[tid >> 1][tid & 1] = 0u;
-  __syncthreads();
-  int item = s_next;
-  if (item < items) issue_stage<RW>(A, decode(A, item, nb), 0, sbase, tid, M);
-  cp_async_commit();
-
-  for (int k = 0; item < items; k++) {
-    const int buf = k & 1;
-    if (tid == 0) s_next = atomicAdd(A.work, 1);
-    __syncthreads();  // B1: previous compute on buffer buf^1 is done; s_next visible
-    const int next = s_next;
-    if (next < items)
-      issue_stage<RW>(A, decode(A, next, nb), 0, sbase + (buf ^ 1) * A.buf_bytes, tid, M);
-    cp_async_commit();
-    cp_async_wait<1>();  // this item's copies (all but the newest group) landed
-    __syncthreads();     // B2: ... for every thread
-
-    const Item it = decode(A, item, nb);
-    const int j0 = it.t * kTile + lane;
-    const bool v0 = j0 < M, v1 = j0 + 32 < M;
-    char *ysm = smem + buf * A.buf_bytes;
-    const uint32_t *rsm = reinterpret_cast<const uint32_t *>(ysm + A.ysm_bytes);
-    uint32_t *alive = s_alive[buf];
-    if (it.nst == 1) {
-      for (int gl = warp; gl < it.ng; gl += kWarps) {
-        const int2 sg = __ldg(reinterpret_cast<const int2 *>(A.L.segs) + it.seg0 + gl);
-        u64 acc[R];
-#pragma unroll
-        for (int r = 0; r < R; r++) acc[r] = 0ull;
-        accumulate<R, FMA>(acc, rsm + (int64_t)sg.x * RW, sg.y, ysm, lane, negz2);
-        epilogue<R, FMA>(A, acc, it.g_first + gl, it.t, lane, v0, v1, alive);
-      }
-    } else {
-      // multi-stage block (plan.cpp: at most kWarps groups, in practice one):
-      // accumulators stay in registers while later stages reload this buffer
-      u64 acc[R];
-#pragma unroll
-      for (int r = 0; r < R; r++) acc[r] = 0ull;
-      for (int s = 0; s < it.nst; s++) {
-        if (s) {
-          __syncthreads();
-          issue_stage<RW>(A, it, s, sbase + buf * A.buf_bytes, tid, M);
-          cp_async_commit();
-          cp_async_wait<0>();
-          __syncthreads();
-        }
-        if (warp < it.ng) {
-          const int2 sg =
-              __ldg(reinterpret_cast<const int2 *>(A.L.segs) + it.seg0 + (int64_t)s * it.ng + warp);
-          accumulate<R, FMA>(acc, rsm + (int64_t)sg.x * RW, sg.y, ysm, lane, negz2);
-        }
-      }
-      if (warp < it.ng) epilogue<R, FMA>(A, acc, it.g_first + warp, it.t, lane, v0, v1, alive);
+  if (tid == 0) {
+    for (int i = 0; i < kBufs; i++) {
+      mbar_init(full0 + 8 * i, 33);                // 32 cp.async arrivals + header
+      mbar_init(empty0 + 8 * i, kConsumerWarps);  // one per consumer warp
+      s_done[i] = 0;
+      for (int w = 0; w < 4; w++) s_alive[i][w] = 0u;
     }
-    __syncthreads();  // B3: every warp's activity bits are in s_alive[buf]
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
 
-    // tile bookkeeping by warp 0 alone; the other warps move on
-    if (warp == 0) {
-      int last = 0, base = 0;
-      u64 mask = 0;
-      if (lane == 0) {
-        const uint32_t lo = alive[0], hi = alive[1];
-        alive[0] = 0u;
-        alive[1] = 0u;
-        if (lo) atomicOr(&A.tile_alive[2 * it.t], lo);
-        if (hi) atomicOr(&A.tile_alive[2 * it.t + 1], hi);
-        __threadfence();
-        const int done = atomicAdd(&A.tile_done[it.t], 1);
-        if (done == nb - 1) {
-          __threadfence();
-          const uint32_t alo = atomicOr(&A.tile_alive[2 * it.t], 0u);
-          const uint32_t ahi = atomicOr(&A.tile_alive[2 * it.t + 1], 0u);
-          mask = (u64)alo | ((u64)ahi << 32);
-          const int cnt = __popcll(mask);
-          base = cnt ? atomicAdd(A.m_out, cnt) : 0;
-          A.tile_done[it.t] = 0;
-          A.tile_alive[2 * it.t] = 0u;
-          A.tile_alive[2 * it.t + 1] = 0u;
-          last = 1;
+  if (warp == kConsumerWarps) {
+    // ======================= producer warp =======================
+    int k = 0;
+    for (;;) {
+      int item = 0;
+      if (lane == 0) item = atomicAdd(A.work, 1);
+      item = __shfl_sync(0xffffffffu, item, 0);
+      const bool more = item < items;
+      int t = 0, b = 0, ng = 0, nst = 1, first_extra = 0;
+      int meta_off = 0, fp_cnt = 0, rec_off = 0, rec_cnt = 0;
+      if (more) {
+        t = item / nb;
+        b = item - t * nb;
+        const int v = lane < 8 ? __ldg(A.L.blocks + (int64_t)b * 8 + lane) : 0;
+        ng = __shfl_sync(0xffffffffu, v, 1);
+        nst = __shfl_sync(0xffffffffu, v, 2);
+        first_extra = __shfl_sync(0xffffffffu, v, 3);
+        meta_off = __shfl_sync(0xffffffffu, v, 4);
+        fp_cnt = __shfl_sync(0xffffffffu, v, 5);
+        rec_off = __shfl_sync(0xffffffffu, v, 6);
+        rec_cnt = __shfl_sync(0xffffffffu, v, 7);
+      }
+      // this lane's four feature columns of tile t
+      int src[4];
+      bool ok[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int j = t * kTile + 4 * lane + q;
+        ok[q] = more && j < M;
+        src[q] = ok[q] ? __ldg(A.a_in + j) : 0;
+      }
+      const bool vec = ok[3] && (src[0] & 3) == 0 && src[1] == src[0] + 1 &&
+                       src[2] == src[0] + 2 && src[3] == src[0] + 3;
+      for (int s = 0; s < (more ? nst : 1); s++) {
+        const int slot = k % kBufs;
+        const uint32_t phase = (uint32_t)(k / kBufs) & 1u;
+        if (s > 0) {
+          const int4 sd = __ldg(reinterpret_cast<const int4 *>(A.L.stages) + first_extra + s - 1);
+          meta_off = sd.x;
+          fp_cnt = sd.y;
+          rec_off = sd.z;
+          rec_cnt = sd.w;
+        }
+        mbar_wait(empty0 + 8 * slot, phase ^ 1u);
+        const uint32_t buf = sbase + slot * A.buf_bytes;
+        const uint32_t smeta = buf + kHeaderBytes;
+        const uint32_t srec = smeta + A.meta_bytes;
+        const uint32_t sy = srec + A.rec_bytes;
+        if (more) {
+          const int meta_words = s == 0 ? (((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3))
+                                        : ((fp_cnt + 3) & ~3);
+          copy_words<4>(smeta, reinterpret_cast<const uint32_t *>(A.L.meta) + meta_off, meta_words,
+                        lane);
+          copy_words<RW>(srec, A.L.records + (int64_t)rec_off * RW, rec_cnt * RW, lane);
+          const int32_t *fp = A.L.meta + meta_off;
+          for (int s0 = 0; s0 < fp_cnt; s0 += 32) {
+            const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
+            const int cnt = min(32, fp_cnt - s0);
+            for (int i = 0; i < cnt; i++) {
+              const int64_t c = __shfl_sync(0xffffffffu, my, i);
+              const float *row = A.y_in + c * A.ld;
+              const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 16 * lane;
+              if (vec) {
+                cp_async16(dst, row + src[0]);
+              } else {
+#pragma unroll
+                for (int q = 0; q < 4; q++) cp_async4(dst + 4 * q, row + src[q], ok[q]);
+              }
+            }
+          }
+        }
+        mbar_cp_async_arrive(full0 + 8 * slot);
+        if (lane == 0) {
+          Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
+          h->item = more ? item : -1;
+          h->t = t;
+          h->b = b;
+          h->stage = s;
+          h->nst = nst;
+          h->ng = ng;
+          h->rec_cnt = rec_cnt;
+          h->fp_cnt = fp_cnt;
+          mbar_arrive(full0 + 8 * slot);
+        }
+        k++;
+      }
+      if (!more) break;
+    }
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  const u64 negz2 = pack2(A.negz, A.negz);
+  u64 acc[2 * R];
+  for (int k = 0;; k++) {
+    const int slot = k % kBufs;
+    const uint32_t phase = (uint32_t)(k / kBufs) & 1u;
+    mbar_wait(full0 + 8 * slot, phase);
+    const char *buf = smem + slot * A.buf_bytes;
+    const Header h = *reinterpret_cast<const Header *>(buf);
+    if (h.item < 0) break;
+    const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
+    const uint32_t *recs = reinterpret_cast<const uint32_t *>(buf + kHeaderBytes + A.meta_bytes);
+    const char *ybase = buf + kHeaderBytes + A.meta_bytes + A.rec_bytes + 16 * lane;
+    const bool last_stage = h.stage == h.nst - 1;
+    if (warp < h.ng) {
+      if (h.stage == 0) {
+#pragma unroll
+        for (int r = 0; r < 2 * R; r++) acc[r] = 0ull;
+      }
+      int rel, cnt;
+      const int seg_base = (h.fp_cnt + 3) & ~3;
+      if (h.nst == 1 || h.stage == 0) {
+        rel = meta[seg_base + 2 * warp];
+        cnt = meta[seg_base + 2 * warp + 1];
+      } else {
+        rel = 0;
+        cnt = h.rec_cnt;
+      }
+      accumulate<R, FMA>(acc, recs + (int64_t)rel * RW, cnt, ybase, negz2);
+      if (last_stage) {
+        // rows live in the stage-0 meta; a multi-stage block's last stage
+        // carries only its fp list, so the rows were captured at stage 0
+        if (h.nst == 1) {
+          const int *rows = meta + seg_base + 2 * h.ng + R * warp;
+          epilogue<R, FMA>(A, acc, rows, h.t, lane, M, s_alive[slot]);
         }
       }
+    }
+    if (h.nst > 1 && last_stage && warp == 0) {
+      // lone multi-stage group: its rows are re-read from global stage-0 meta
+      const int32_t *blk = A.L.blocks + (int64_t)h.b * 8;
+      const int fp0 = __ldg(blk + 5);
+      const int *rows = A.L.meta + __ldg(blk + 4) + ((fp0 + 3) & ~3) + 2;
+      int rr[R];
+#pragma unroll
+      for (int r = 0; r < R; r++) rr[r] = __ldg(rows + r);
+      epilogue<R, FMA>(A, acc, rr, h.t, lane, M, s_alive[slot]);
+    }
+    __syncwarp();
+    int bookkeeper = 0;
+    if (last_stage) {
+      if (lane == 0) {
+        __threadfence_block();
+        bookkeeper = atomicAdd(&s_done[slot], 1) == kConsumerWarps - 1;
+      }
+      bookkeeper = __shfl_sync(0xffffffffu, bookkeeper, 0);
+    }
+    if (bookkeeper) {
+      // every consumer warp has published its activity bits for this item
+      __threadfence_block();
+      uint32_t w4 = lane < 4 ? s_alive[slot][lane] : 0u;
+      __syncwarp();
+      if (lane < 4) s_alive[slot][lane] = 0u;
+      if (lane == 0) s_done[slot] = 0;
+      int last = 0;
+      if (lane < 4 && w4) atomicOr(&A.tile_alive[4 * h.t + lane], w4);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) last = atomicAdd(&A.tile_done[h.t], 1) == nb - 1;
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
+        __threadfence();
+        if (lane < 4) {
+          w4 = atomicOr(&A.tile_alive[4 * h.t + lane], 0u);
+          A.tile_alive[4 * h.t + lane] = 0u;
+        }
+        if (lane == 0) A.tile_done[h.t] = 0;
+        const uint32_t m0 = __shfl_sync(0xffffffffu, w4, 0), m1 = __shfl_sync(0xffffffffu, w4, 1);
+        const uint32_t m2 = __shfl_sync(0xffffffffu, w4, 2), m3 = __shfl_sync(0xffffffffu, w4, 3);
+        const int c0 = __popc(m0), c1 = __popc(m1), c2 = __popc(m2), c3 = __popc(m3);
+        int base = 0;
+        if (lane == 0 && c0 + c1 + c2 + c3) base = atomicAdd(A.m_out, c0 + c1 + c2 + c3);
         base = __shfl_sync(0xffffffffu, base, 0);
-        mask = __shfl_sync(0xffffffffu, mask, 0);
+        const uint32_t mw[4] = {m0, m1, m2, m3};
+        const int pre[4] = {0, c0, c0 + c1, c0 + c1 + c2};
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const int f = lane + 32 * h;
-          if ((mask >> f) & 1ull) {
-            const int rank = __popcll(mask & ((1ull << f) - 1ull));
-            const int j = it.t * kTile + f;
+        for (int w = 0; w < 4; w++) {
+          if ((mw[w] >> lane) & 1u) {
+            const int rank = pre[w] + __popc(mw[w] & ((1u << lane) - 1u));
+            const int j = h.t * kTile + 32 * w + lane;
             A.a_out[base + rank] = j;
             A.cat_out[base + rank] = A.cat_in[j];
           }
         }
       }
     }
-    item = next;
+    if (lane == 0) mbar_arrive(empty0 + 8 * slot);
   }
-  cp_async_wait<0>();
 }
 
 // ---- launch configuration ---------------------------------------------------
@@ -414,18 +527,23 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   int sms;
   size_t optin;
   if (device_info(sms, optin)) return spdnn_fail(SPDNN_ECUDA, "layer: no CUDA device");
-  const size_t ysm = (size_t)L.max_fp_per_stage * kTile * 4;
-  const size_t rsm = ((size_t)L.max_records_per_stage * L.record_words * 4 + 15) / 16 * 16;
-  const size_t buf = (ysm + rsm + 127) / 128 * 128;
-  const size_t smem = 2 * buf;
-  if (smem + 1024 > optin) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
-  A.ysm_bytes = (uint32_t)ysm;
+  auto up16 = [](size_t x) { return (x + 15) / 16 * 16; };
+  const size_t meta = up16((size_t)L.max_meta_per_block * 4);
+  const size_t rec = up16((size_t)L.max_records_per_stage * L.record_words * 4);
+  const size_t ys = (size_t)L.max_fp_per_stage * kRowBytes;
+  const size_t buf = (kHeaderBytes + meta + rec + ys + 127) / 128 * 128;
+  const size_t smem = kBufs * buf;
+  if (smem + 2048 > optin)
+    return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
+  A.meta_bytes = (uint32_t)meta;
+  A.rec_bytes = (uint32_t)rec;
   A.buf_bytes = (uint32_t)buf;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem);
-  if (e != cudaSuccess || per_sm < 1) return spdnn_fail(SPDNN_ECUDA, "layer: kernel does not fit on an SM");
+  if (e != cudaSuccess || per_sm < 1)
+    return spdnn_fail(SPDNN_ECUDA, "layer: kernel does not fit on an SM");
   void *args[] = {&A};
   e = cudaLaunchKernel(fn, dim3(sms * per_sm), dim3(kThreads), args, smem, stream);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
@@ -515,8 +633,7 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   A.guard = scratch->guard;
   A.tiny = opts ? opts->tiny : 0.0f;
   A.negz = -0.0f;
-  A.buf_bytes = 0;
-  A.ysm_bytes = 0;
+  A.buf_bytes = A.meta_bytes = A.rec_bytes = 0;
   if (A.L.num_blocks == 0) return SPDNN_OK;  // N == 0
   return launch_layer(A, fma, (cudaStream_t)stream);
 }
@@ -577,6 +694,6 @@ extern "C" int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_s
                                      int32_t *threads_per_cta) {
   (void)rows_per_group;
   if (threads_per_cta) *threads_per_cta = kThreads;
-  if (ctas_per_sm) *ctas_per_sm = 0;
+  if (ctas_per_sm) *ctas_per_sm = 1;
   return SPDNN_OK;
 }

@@ -23,6 +23,8 @@
 #include <cstdint>
 #include <cstring>
 #include <new>
+#include <stdexcept>
+#include <utility>
 #include <string>
 #include <thread>
 #include <vector>
@@ -32,22 +34,20 @@
 struct spdnn_plan {
   int64_t n = 0;
   int R = 1, RW = 2;
-  std::vector<int32_t> blocks;   // 8 ints per block
-  std::vector<int64_t> stages;   // 4 per stage
-  std::vector<int32_t> segs;     // 2 per seg
-  std::vector<int32_t> fp;
-  std::vector<int32_t> rows;
+  std::vector<int32_t> blocks;   // 8 ints per block (descriptor)
+  std::vector<int32_t> stages;   // 4 ints per extra stage of a multi-stage block
+  std::vector<int32_t> meta;     // per block: fp list, group segments, group rows
   std::vector<uint32_t> records;
   int64_t nnz = 0;
   int64_t num_groups = 0;
-  int32_t max_fp = 0, max_rec = 0;
+  int32_t max_fp = 0, max_rec = 0, max_meta = 0;
+  int64_t num_fp = 0;
   int32_t pow2 = 0;              // every nonzero weight is +-2^e (FMA form allowed)
   int32_t wexp_min = 0, wexp_max = 0;
 };
 
 namespace {
 
-constexpr int kTileBytes = 64 * 4;  // one staged input neuron: 64 fp32 features
 
 int record_words(int R) { return R == 1 ? 2 : (R == 3 ? 4 : 8); }
 
@@ -180,6 +180,16 @@ int64_t total_records(const std::vector<Group> &gs) {
 // 4 wavefronts. Time ~ max(issue/4, wavefronts) smem-or-issue bound per SM.
 double record_cost(int R) { return R == 1 ? 3.0 : (R == 3 ? 3.0 : 4.25); }
 
+void pad4(std::vector<int32_t> &v) {
+  while (v.size() % 4) v.push_back(0);
+}
+
+// Lay the groups out as blocks. Per block (include/spdnn_b200.h):
+//   descriptor {g_first, ng, nst, first_extra_stage, meta_off, fp_cnt, rec_off, rec_cnt}
+//   meta       [fp indices of stage 0][pad][ng x (rec_rel, cnt)][ng x R rows][pad]
+//   records    per group, its union columns in ascending order
+// A block with more than one stage holds exactly one group; its stages 1..
+// live in `stages` as {meta_off, fp_cnt, rec_off, rec_cnt} (meta = fp list).
 void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
           const std::vector<Group> &gs, const spdnn_plan_params &p) {
   const int R = pl->R, RW = pl->RW;
@@ -189,21 +199,51 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
   std::vector<int32_t> slot_of(n, 0);
   std::vector<int32_t> fp_block;
   int32_t blk_id = 0;
-  // weight lookup for one row and column: rows are sorted, use binary search
   auto weight = [&](int32_t row, int32_t col) -> float {
     const int32_t *b = ci + rp[row], *e = ci + rp[row + 1];
     const int32_t *it = std::lower_bound(b, e, col);
     return (it != e && *it == col) ? va[it - ci] : 0.0f;
   };
-
-  pl->rows.resize(gs.size() * R);
-  for (size_t g = 0; g < gs.size(); g++)
-    for (int k = 0; k < R; k++) pl->rows[g * R + k] = gs[g].rows[k];
+  // records of groups [g0, g0+ng) restricted to footprint columns [c_lo, c_hi)
+  auto emit_records = [&](size_t g0, size_t ng, int64_t c_lo, int64_t c_hi,
+                          std::vector<int32_t> *gseg) {
+    const int32_t lo_col = c_hi > c_lo ? fp_block[c_lo] : 0;
+    const int32_t hi_col = c_hi > c_lo ? fp_block[c_hi - 1] : -1;
+    for (int64_t i = c_lo; i < c_hi; i++) slot_of[fp_block[i]] = (int32_t)(i - c_lo);
+    const int64_t rec_off = (int64_t)pl->records.size() / RW;
+    for (size_t gg = g0; gg < g0 + ng; gg++) {
+      const int64_t start = (int64_t)pl->records.size() / RW - rec_off;
+      int64_t cnt = 0;
+      for (int32_t c : gs[gg].cols) {
+        if (c < lo_col || c > hi_col) continue;
+        const size_t base = pl->records.size();
+        pl->records.resize(base + RW, 0u);
+        pl->records[base] = (uint32_t)slot_of[c] * (uint32_t)SPDNN_STAGED_ROW_BYTES;
+        for (int k = 0; k < R; k++) {
+          const int32_t row = gs[gg].rows[k];
+          const float w = row >= 0 ? weight(row, c) : 0.0f;
+          uint32_t bits;
+          std::memcpy(&bits, &w, 4);
+          pl->records[base + 1 + k] = bits;
+        }
+        cnt++;
+      }
+      if (gseg) {
+        gseg->push_back((int32_t)start);
+        gseg->push_back((int32_t)cnt);
+      }
+    }
+    const int64_t rec_cnt = (int64_t)pl->records.size() / RW - rec_off;
+    pl->max_rec = std::max<int32_t>(pl->max_rec, (int32_t)rec_cnt);
+    pl->max_fp = std::max<int32_t>(pl->max_fp, (int32_t)(c_hi - c_lo));
+    return std::make_pair(rec_off, rec_cnt);
+  };
 
   size_t g = 0;
+  std::vector<int32_t> gseg;
   while (g < gs.size()) {
     // ---- choose the block's groups
-    size_t g0 = g;
+    const size_t g0 = g;
     fp_block.clear();
     int64_t recs = 0;
     while (g < gs.size() && (int64_t)(g - g0) < GMAX) {
@@ -217,65 +257,43 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
       recs += (int64_t)gs[g].cols.size();
       g++;
     }
-    size_t ng = g - g0;
+    const size_t ng = g - g0;
     std::sort(fp_block.begin(), fp_block.end());
-    // ---- stages: one unless a lone group overflows the caps
-    int64_t nfp = (int64_t)fp_block.size();
-    int64_t nst = 1;
-    if (nfp > S || recs > RC) nst = (nfp + S - 1) / S;  // ng == 1 here
-    if (nst > 1 && ng != 1) nst = 1;  // cannot happen by construction
-    int64_t first_stage = (int64_t)pl->stages.size() / 4;
-    int64_t first_seg = (int64_t)pl->segs.size() / 2;
-    int32_t *blk = nullptr;
-    pl->blocks.resize(pl->blocks.size() + 8, 0);
-    blk = pl->blocks.data() + pl->blocks.size() - 8;
-    blk[0] = (int32_t)g0;
-    blk[1] = (int32_t)ng;
-    blk[2] = (int32_t)first_stage;
-    blk[3] = (int32_t)nst;
-    blk[4] = (int32_t)(first_seg & 0xffffffff);
-    blk[5] = (int32_t)(first_seg >> 32);
-    for (int64_t s = 0; s < nst; s++) {
-      int64_t c_lo = s * S, c_hi = std::min<int64_t>(nfp, (s + 1) * S);
-      if (nst == 1) { c_lo = 0; c_hi = nfp; }
-      int64_t fp_off = (int64_t)pl->fp.size();
-      for (int64_t i = c_lo; i < c_hi; i++) {
-        pl->fp.push_back(fp_block[i]);
-        slot_of[fp_block[i]] = (int32_t)(i - c_lo);
-      }
-      int64_t rec_off = (int64_t)pl->records.size() / RW;
-      const int32_t lo_col = c_hi > c_lo ? fp_block[c_lo] : 0;
-      const int32_t hi_col = c_hi > c_lo ? fp_block[c_hi - 1] : -1;
-      for (size_t gg = g0; gg < g0 + ng; gg++) {
-        int64_t seg_start = (int64_t)pl->records.size() / RW - rec_off;
-        int64_t cntr = 0;
-        for (int32_t c : gs[gg].cols) {
-          if (c < lo_col || c > hi_col) continue;
-          size_t base = pl->records.size();
-          pl->records.resize(base + RW, 0u);
-          pl->records[base] = (uint32_t)slot_of[c] * (uint32_t)kTileBytes;
-          for (int k = 0; k < R; k++) {
-            int32_t row = gs[gg].rows[k];
-            float w = row >= 0 ? weight(row, c) : 0.0f;
-            uint32_t bits;
-            std::memcpy(&bits, &w, 4);
-            pl->records[base + 1 + k] = bits;
-          }
-          cntr++;
-        }
-        pl->segs.push_back((int32_t)seg_start);
-        pl->segs.push_back((int32_t)cntr);
-      }
-      int64_t rec_cnt = (int64_t)pl->records.size() / RW - rec_off;
-      pl->stages.push_back(fp_off);
-      pl->stages.push_back(c_hi - c_lo);
-      pl->stages.push_back(rec_off);
-      pl->stages.push_back(rec_cnt);
-      pl->max_fp = std::max<int32_t>(pl->max_fp, (int32_t)(c_hi - c_lo));
-      pl->max_rec = std::max<int32_t>(pl->max_rec, (int32_t)rec_cnt);
+    const int64_t nfp = (int64_t)fp_block.size();
+    // a block overflows the caps only when it is a lone group (loop above)
+    const int64_t nst = (nfp > S || recs > RC) ? (nfp + S - 1) / S : 1;
+    // ---- stage 0: descriptor + meta + records
+    const int64_t c_hi0 = nst == 1 ? nfp : std::min<int64_t>(nfp, S);
+    const int64_t meta_off = (int64_t)pl->meta.size();
+    pl->meta.insert(pl->meta.end(), fp_block.begin(), fp_block.begin() + c_hi0);
+    pad4(pl->meta);
+    gseg.clear();
+    auto r0 = emit_records(g0, ng, 0, c_hi0, &gseg);
+    pl->meta.insert(pl->meta.end(), gseg.begin(), gseg.end());
+    for (size_t gg = g0; gg < g0 + ng; gg++)
+      for (int k = 0; k < R; k++) pl->meta.push_back(gs[gg].rows[k]);
+    pad4(pl->meta);
+    pl->max_meta = std::max<int32_t>(pl->max_meta, (int32_t)(pl->meta.size() - meta_off));
+    const int64_t first_extra = (int64_t)pl->stages.size() / 4;
+    const int32_t desc[8] = {(int32_t)g0, (int32_t)ng, (int32_t)nst, (int32_t)first_extra,
+                             (int32_t)meta_off, (int32_t)c_hi0, (int32_t)r0.first,
+                             (int32_t)r0.second};
+    pl->blocks.insert(pl->blocks.end(), desc, desc + 8);
+    // ---- further stages of a lone oversized group
+    for (int64_t st = 1; st < nst; st++) {
+      const int64_t c_lo = st * S, c_hi = std::min<int64_t>(nfp, (st + 1) * S);
+      const int64_t moff = (int64_t)pl->meta.size();
+      pl->meta.insert(pl->meta.end(), fp_block.begin() + c_lo, fp_block.begin() + c_hi);
+      pad4(pl->meta);
+      auto r = emit_records(g0, ng, c_lo, c_hi, nullptr);
+      const int32_t sd[4] = {(int32_t)moff, (int32_t)(c_hi - c_lo), (int32_t)r.first,
+                             (int32_t)r.second};
+      pl->stages.insert(pl->stages.end(), sd, sd + 4);
     }
     blk_id++;
   }
+  if (pl->meta.size() >= ((size_t)1 << 31) || pl->records.size() / RW >= ((size_t)1 << 31))
+    throw std::length_error("layer layout exceeds 2^31 entries");
 }
 
 }  // namespace
@@ -295,7 +313,7 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
     return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: rows_per_group must be 0, 1, 3 or 7");
   if (n > 0 && !valid_csr(n, row_ptr, col_idx))
     return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: CSR is not canonical");
-  if ((int64_t)p.footprint_cap * kTileBytes >= (int64_t)1 << 32)
+  if ((int64_t)p.footprint_cap * SPDNN_STAGED_ROW_BYTES >= (int64_t)1 << 31)
     return spdnn_fail(SPDNN_ERANGE, "spdnn_plan_build: footprint cap too large");
   spdnn_plan *pl = new (std::nothrow) spdnn_plan();
   if (!pl) return spdnn_fail(SPDNN_ENOMEM, "spdnn_plan_build: out of memory");
@@ -331,6 +349,9 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
   } catch (const std::bad_alloc &) {
     delete pl;
     return spdnn_fail(SPDNN_ENOMEM, "spdnn_plan_build: out of memory");
+  } catch (const std::length_error &) {
+    delete pl;
+    return spdnn_fail(SPDNN_ERANGE, "spdnn_plan_build: layer layout exceeds 2^31 entries");
   }
   *out = pl;
   return SPDNN_OK;
@@ -376,33 +397,33 @@ extern "C" int spdnn_plan_sizes(const spdnn_plan *pl, spdnn_plan_sizes_t *s) {
   s->rows_per_group = pl->R;
   s->record_words = pl->RW;
   s->num_blocks = (int64_t)pl->blocks.size() / 8;
-  s->num_stages = (int64_t)pl->stages.size() / 4;
+  s->num_extra_stages = (int64_t)pl->stages.size() / 4;
   s->num_groups = pl->num_groups;
-  s->num_segs = (int64_t)pl->segs.size() / 2;
-  s->num_fp = (int64_t)pl->fp.size();
+  s->num_meta = (int64_t)pl->meta.size();
   s->num_records = (int64_t)pl->records.size() / pl->RW;
+  s->num_fp = 0;
+  for (size_t b = 0; b < pl->blocks.size(); b += 8) s->num_fp += pl->blocks[b + 5];
+  for (size_t st = 0; st < pl->stages.size(); st += 4) s->num_fp += pl->stages[st + 1];
   s->nnz = pl->nnz;
   s->padded_slots = s->num_records * pl->R;
   s->max_fp_per_stage = pl->max_fp;
   s->max_records_per_stage = pl->max_rec;
+  s->max_meta_per_block = pl->max_meta;
   s->pow2 = pl->pow2;
   s->wexp_min = pl->wexp_min;
   s->wexp_max = pl->wexp_max;
   return SPDNN_OK;
 }
 
-extern "C" int spdnn_plan_export(const spdnn_plan *pl, int32_t *blocks, int64_t *stages,
-                                 int32_t *segs, int32_t *fp, int32_t *rows,
-                                 uint32_t *records) {
+extern "C" int spdnn_plan_export(const spdnn_plan *pl, int32_t *blocks, int32_t *stages,
+                                 int32_t *meta, uint32_t *records) {
   if (!pl) return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_export: null plan");
   auto cp = [](auto *dst, const auto &v) {
     if (!v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
   };
   cp(blocks, pl->blocks);
   cp(stages, pl->stages);
-  cp(segs, pl->segs);
-  cp(fp, pl->fp);
-  cp(rows, pl->rows);
+  cp(meta, pl->meta);
   cp(records, pl->records);
   return SPDNN_OK;
 }

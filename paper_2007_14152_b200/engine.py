@@ -38,7 +38,7 @@ from .model import (FeatureBatch, InferenceConfig, LayerCSR, ModelError, Network
                     count_edges)
 
 Mode = Literal["baseline", "optimized"]
-TILE = 64
+TILE = 128  # features per work item (include/spdnn_b200.h SPDNN_TILE_FEATURES)
 
 
 # ---------------------------------------------------------------------------
@@ -73,9 +73,9 @@ class InferenceResult:
 class PlanParams:
     """Kernel geometry knobs of the row-grouped union layout."""
     rows_per_group: int = 0      # 0 = cost model picks 1, 3 or 7 per layer
-    footprint_cap: int = 192     # staged input neurons per block stage (x256 B smem)
+    footprint_cap: int = 160     # staged input neurons per block stage (x512 B smem)
     max_groups: int = 16         # row groups per block (one per warp)
-    record_cap: int = 1024       # union records per block stage
+    record_cap: int = 640        # union records per block stage
     reorder: bool = True
 
 
@@ -104,14 +104,13 @@ class LayerPlan:
     num_blocks: int
     max_fp_per_stage: int
     max_records_per_stage: int
+    max_meta_per_block: int
     num_records: int
     num_fp: int
-    blocks: np.ndarray
-    stages: np.ndarray
-    segs: np.ndarray
-    fp: np.ndarray
-    rows: np.ndarray
-    records: np.ndarray
+    blocks: np.ndarray    # int32 [num_blocks, 8] descriptors
+    stages: np.ndarray    # int32 [num_extra_stages, 4]
+    meta: np.ndarray      # int32 per-block fp lists / group segments / rows
+    records: np.ndarray   # uint32 [num_records * record_words]
 
     @property
     def total_slots(self) -> int:
@@ -138,22 +137,20 @@ def _export(handle) -> LayerPlan:
     _native.check(L.spdnn_plan_sizes(handle, ctypes.byref(s)), "spdnn_plan_sizes")
     arrs = dict(
         blocks=np.zeros(s.num_blocks * 8, np.int32),
-        stages=np.zeros(s.num_stages * 4, np.int64),
-        segs=np.zeros(s.num_segs * 2, np.int32),
-        fp=np.zeros(s.num_fp, np.int32),
-        rows=np.zeros(s.num_groups * s.rows_per_group, np.int32),
+        stages=np.zeros(s.num_extra_stages * 4, np.int32),
+        meta=np.zeros(s.num_meta, np.int32),
         records=np.zeros(s.num_records * s.record_words, np.uint32),
     )
     ptr = lambda a: ctypes.c_void_p(a.ctypes.data)
     _native.check(L.spdnn_plan_export(handle, ptr(arrs["blocks"]), ptr(arrs["stages"]),
-                                      ptr(arrs["segs"]), ptr(arrs["fp"]),
-                                      ptr(arrs["rows"]), ptr(arrs["records"])),
+                                      ptr(arrs["meta"]), ptr(arrs["records"])),
                   "spdnn_plan_export")
     return LayerPlan(neurons=s.neurons, rows_per_group=s.rows_per_group,
                      record_words=s.record_words, pow2=bool(s.pow2),
                      wexp_min=s.wexp_min, wexp_max=s.wexp_max,
                      num_blocks=s.num_blocks, max_fp_per_stage=s.max_fp_per_stage,
                      max_records_per_stage=s.max_records_per_stage,
+                     max_meta_per_block=s.max_meta_per_block,
                      num_records=s.num_records, num_fp=s.num_fp, **arrs)
 
 
@@ -247,7 +244,7 @@ class DeviceNetwork:
         self.neurons = int(bias.shape[0])
         self.modes = {p.mode for p in prepared}
         plans = [p.plan for p in prepared]
-        kinds = ("blocks", "stages", "segs", "fp", "rows", "records")
+        kinds = ("blocks", "stages", "meta", "records")
         self.buffers = {}
         offsets = {k: [] for k in kinds}
         for k in kinds:
@@ -280,6 +277,7 @@ class DeviceNetwork:
             d.record_words = pl.record_words
             d.max_fp_per_stage = pl.max_fp_per_stage
             d.max_records_per_stage = pl.max_records_per_stage
+            d.max_meta_per_block = pl.max_meta_per_block
         # FMA form (one FFMA2 per (row, column)) is exact when every weight is
         # +-2^e and no input falls below `tiny` (products stay normal) or above
         # `huge` (no overflow); the kernels flag violations and infer() reruns
@@ -312,7 +310,7 @@ class Workspace:
         self.counts = torch.zeros(num_layers + 1, dtype=i32, device=device)
         tiles = self.ld // TILE
         self.tile_done = torch.zeros(tiles, dtype=i32, device=device)
-        self.tile_alive = torch.zeros(2 * tiles, dtype=i32, device=device)
+        self.tile_alive = torch.zeros(4 * tiles, dtype=i32, device=device)
         self.work = torch.zeros(max(1, num_layers), dtype=i32, device=device)
         self.guard = torch.zeros(1, dtype=i32, device=device)
         self.scratch = _native.Scratch(self.tile_done.data_ptr(), self.tile_alive.data_ptr(),

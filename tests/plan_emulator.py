@@ -1,10 +1,42 @@
 """CPU re-execution of a LayerPlan in the exact order and rounding the CUDA
 kernel uses (csrc/layer.cu). Test infrastructure: lets the layout builder be
 checked bit-for-bit against the oracle without a GPU. float32 numpy ops are
-IEEE single precision with round-to-nearest, like mul.rn / add.rn / fma.rn
-with an exact product."""
+IEEE single precision with round-to-nearest, like the kernel's fma.rn with
+an exact product / add.rn."""
 
 import numpy as np
+
+ROW_BYTES = 512  # SPDNN_STAGED_ROW_BYTES
+
+
+def r4(x):
+    return (x + 3) & ~3
+
+
+def decode(plan):
+    """Yield, per block: (stages, groups) with stages = [(fp list, records)],
+    groups = [(rows, [(stage, rel, cnt)])]."""
+    R, RW = plan.rows_per_group, plan.record_words
+    rec = plan.records.reshape(-1, RW) if plan.num_records else np.zeros((0, RW), np.uint32)
+    blocks = plan.blocks.reshape(-1, 8)
+    extra = plan.stages.reshape(-1, 4)
+    for g0, ng, nst, first_extra, meta_off, fp_cnt, rec_off, rec_cnt in blocks:
+        meta = plan.meta
+        fp = meta[meta_off:meta_off + fp_cnt]
+        seg = meta[meta_off + r4(fp_cnt): meta_off + r4(fp_cnt) + 2 * ng].reshape(-1, 2)
+        rows = meta[meta_off + r4(fp_cnt) + 2 * ng: meta_off + r4(fp_cnt) + 2 * ng + R * ng]
+        stages = [(fp, rec[rec_off:rec_off + rec_cnt])]
+        for s in range(1, nst):
+            moff, fc, ro, rc = extra[first_extra + s - 1]
+            stages.append((meta[moff:moff + fc], rec[ro:ro + rc]))
+        groups = []
+        for gl in range(ng):
+            segs = [(0, int(seg[gl, 0]), int(seg[gl, 1]))]
+            if nst > 1:
+                assert ng == 1
+                segs += [(s, 0, len(stages[s][1])) for s in range(1, nst)]
+            groups.append((rows[gl * R:(gl + 1) * R], segs))
+        yield stages, groups
 
 
 def emulate_layer(plan, bias, x):
@@ -12,34 +44,24 @@ def emulate_layer(plan, bias, x):
     n, m = x.shape
     out = np.empty((n, m), dtype=np.float32, order="F")
     written = np.zeros(n, dtype=bool)
-    R, RW = plan.rows_per_group, plan.record_words
-    rec = plan.records.reshape(-1, RW) if plan.num_records else np.zeros((0, RW), np.uint32)
-    blocks = plan.blocks.reshape(-1, 8)
-    stages = plan.stages.reshape(-1, 4)
-    segs = plan.segs.reshape(-1, 2)
+    R = plan.rows_per_group
     x = np.asarray(x, dtype=np.float32)
-    for b in range(plan.num_blocks):
-        g0, ng, s0, ns, lo, hi = (int(v) for v in blocks[b][:6])
-        seg0 = (lo & 0xffffffff) | (hi << 32)
-        acc = np.zeros((ng, R, m), dtype=np.float32)
-        for s in range(ns):
-            fp_off, fp_cnt, rec_off, rec_cnt = (int(v) for v in stages[s0 + s])
-            cols = plan.fp[fp_off:fp_off + fp_cnt]
-            for gl in range(ng):
-                so, sc = (int(v) for v in segs[seg0 + s * ng + gl])
-                for r in rec[rec_off + so: rec_off + so + sc]:
-                    slot = int(r[0]) // 256
-                    y = x[cols[slot]]
+    for stages, groups in decode(plan):
+        for rows, segs in groups:
+            acc = np.zeros((R, m), dtype=np.float32)
+            for s, rel, cnt in segs:
+                fp, recs = stages[s]
+                for r in recs[rel:rel + cnt]:
+                    assert int(r[0]) % ROW_BYTES == 0
+                    y = x[fp[int(r[0]) // ROW_BYTES]]
                     ws = r[1:1 + R].view(np.float32)
                     for k in range(R):
-                        p = (y * ws[k]).astype(np.float32)
-                        acc[gl, k] = acc[gl, k] + p
-        for gl in range(ng):
+                        acc[k] = acc[k] + (y * ws[k]).astype(np.float32)
             for k in range(R):
-                row = int(plan.rows[(g0 + gl) * R + k])
+                row = int(rows[k])
                 if row < 0:
                     continue
-                v = (acc[gl, k] + np.float32(bias[row])).astype(np.float32)
+                v = (acc[k] + np.float32(bias[row])).astype(np.float32)
                 v = np.where(v < 0, np.float32(0), v)
                 v = np.where(v > 32, np.float32(32), v)
                 out[row] = v
