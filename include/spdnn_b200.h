@@ -75,10 +75,11 @@ typedef struct spdnn_plan_sizes_t {
   int64_t num_extra_stages; /* stages beyond the first of multi-stage blocks */
   int64_t num_groups;
   int64_t num_meta;         /* int32 words of per-block metadata */
-  int64_t num_records;      /* union records (one per (group, input neuron)) */
+  int64_t num_records;      /* records array length (union records + 16-byte
+                               alignment padding of R = 1 stages) */
   int64_t num_fp;           /* staged input neurons, summed over all stages */
   int64_t nnz;
-  int64_t padded_slots;     /* num_records * R: multiply-add slots per feature */
+  int64_t padded_slots;     /* union records * R: multiply-add slots per feature */
   int32_t max_fp_per_stage;
   int32_t max_records_per_stage;
   int32_t max_meta_per_block;

@@ -85,12 +85,6 @@ __device__ __forceinline__ void cp_async4(uint32_t saddr, const void *gmem, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(saddr), "l"(gmem),
                "r"(valid ? 4 : 0));
 }
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async8(uint32_t saddr, const void *gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
-}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
 }
@@ -98,19 +92,34 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar)
                : "memory");
 }
-// arrives on `bar` when all prior cp.async of this thread have landed
-__device__ __forceinline__ void mbar_cp_async_arrive(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
+// Blocks (suspended, up to the time hint) until the phase with `parity` is done.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"
       " .reg .pred p;\n"
       "WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n"
       "}\n" ::"r"(bar),
-      "r"(parity)
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+// cp.async.mbarrier.arrive (counted): +1 pending now, -1 when this thread's
+// earlier cp.async copies have landed
+__device__ __forceinline__ void mbar_cp_async_arrive_inc(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+// TMA bulk copy global -> this CTA's shared memory, completion as tx bytes
+__device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+      ::"r"(sdst), "l"(gsrc), "r"(bytes), "r"(bar)
       : "memory");
 }
 
@@ -254,18 +263,6 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, con
   if (FMA && tiny) atomicOr(A.guard, 1u);
 }
 
-// Contiguous words -> smem: 16-byte chunks when the source is 16-byte
-// aligned (ALIGN_WORDS = 4: meta, R = 3 / 7 records), else 8-byte chunks.
-template <int ALIGN_WORDS>
-__device__ __forceinline__ void copy_words(uint32_t sdst, const uint32_t *src, int words,
-                                           int lane) {
-  if (ALIGN_WORDS >= 4) {
-    for (int i = lane; i < (words >> 2); i += 32) cp_async16(sdst + 16 * i, src + 4 * i);
-  } else {
-    for (int i = lane; i < (words >> 1); i += 32) cp_async8(sdst + 8 * i, src + 2 * i);
-  }
-}
-
 template <int R, bool FMA>
 __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
@@ -286,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
 
   if (tid == 0) {
     for (int i = 0; i < kBufs; i++) {
-      mbar_init(full0 + 8 * i, 33);                // 32 cp.async arrivals + header
+      mbar_init(full0 + 8 * i, 1);                 // the header arrival (+ tx bytes)
       mbar_init(empty0 + 8 * i, kConsumerWarps);  // one per consumer warp
       s_done[i] = 0;
       for (int w = 0; w < 4; w++) s_alive[i][w] = 0u;
@@ -297,6 +294,11 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
 
   if (warp == kConsumerWarps) {
     // ======================= producer warp =======================
+    // Per ring fill: TMA bulk copies for the block metadata, the union
+    // records and -- when the tile's 128 feature columns are contiguous (the
+    // steady state; every tile right after a death-free layer) -- one 512-byte
+    // row per staged input neuron. Tiles holding gaps left by features that
+    // died in the previous layer are gathered with 4-byte cp.async instead.
     int k = 0;
     for (;;) {
       int item = 0;
@@ -318,16 +320,20 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
         rec_cnt = __shfl_sync(0xffffffffu, v, 7);
       }
       // this lane's four feature columns of tile t
+      const int valid = more ? min(kTile, M - t * kTile) : 0;
       int src[4];
       bool ok[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const int j = t * kTile + 4 * lane + q;
-        ok[q] = more && j < M;
-        src[q] = ok[q] ? __ldg(A.a_in + j) : 0;
+        const int f = 4 * lane + q;
+        ok[q] = f < valid;
+        src[q] = ok[q] ? __ldg(A.a_in + t * kTile + f) : 0;
       }
-      const bool vec = ok[3] && (src[0] & 3) == 0 && src[1] == src[0] + 1 &&
-                       src[2] == src[0] + 2 && src[3] == src[0] + 3;
+      const int p0 = __shfl_sync(0xffffffffu, src[0], 0);
+      const bool mine_contig = (!ok[0] || src[0] == p0 + 4 * lane) && (!ok[1] || src[1] == p0 + 4 * lane + 1) &&
+                               (!ok[2] || src[2] == p0 + 4 * lane + 2) && (!ok[3] || src[3] == p0 + 4 * lane + 3);
+      const bool contig = __all_sync(0xffffffffu, mine_contig) && (p0 & 3) == 0;
+      const uint32_t row_bytes = (uint32_t)((valid + 3) & ~3) * 4u;
       for (int s = 0; s < (more ? nst : 1); s++) {
         const int slot = k % kBufs;
         const uint32_t phase = (uint32_t)(k / kBufs) & 1u;
@@ -339,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
           rec_cnt = sd.w;
         }
         mbar_wait(empty0 + 8 * slot, phase ^ 1u);
+        const uint32_t full = full0 + 8 * slot;
         const uint32_t buf = sbase + slot * A.buf_bytes;
         const uint32_t smeta = buf + kHeaderBytes;
         const uint32_t srec = smeta + A.meta_bytes;
@@ -346,27 +353,35 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
         if (more) {
           const int meta_words = s == 0 ? (((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3))
                                         : ((fp_cnt + 3) & ~3);
-          copy_words<4>(smeta, reinterpret_cast<const uint32_t *>(A.L.meta) + meta_off, meta_words,
-                        lane);
-          copy_words<RW>(srec, A.L.records + (int64_t)rec_off * RW, rec_cnt * RW, lane);
+          const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
+          const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
+                              (contig ? (uint32_t)fp_cnt * row_bytes : 0u);
+          if (lane == 0) mbar_expect_tx(full, tx);
+          __syncwarp();
+          if (lane == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
+          if (lane == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
           const int32_t *fp = A.L.meta + meta_off;
-          for (int s0 = 0; s0 < fp_cnt; s0 += 32) {
-            const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
-            const int cnt = min(32, fp_cnt - s0);
-            for (int i = 0; i < cnt; i++) {
-              const int64_t c = __shfl_sync(0xffffffffu, my, i);
-              const float *row = A.y_in + c * A.ld;
-              const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 16 * lane;
-              if (vec) {
-                cp_async16(dst, row + src[0]);
-              } else {
+          if (contig) {
+            for (int i = lane; i < fp_cnt; i += 32) {
+              const int64_t c = __ldg(fp + i);
+              bulk_g2s(sy + (uint32_t)i * kRowBytes, A.y_in + c * A.ld + p0, row_bytes, full);
+            }
+          } else {
+            for (int s0 = 0; s0 < fp_cnt; s0 += 32) {
+              const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
+              const int cnt = min(32, fp_cnt - s0);
+              for (int i = 0; i < cnt; i++) {
+                const int64_t c = __shfl_sync(0xffffffffu, my, i);
+                const float *row = A.y_in + c * A.ld;
+                const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 16 * lane;
 #pragma unroll
                 for (int q = 0; q < 4; q++) cp_async4(dst + 4 * q, row + src[q], ok[q]);
               }
             }
+            mbar_cp_async_arrive_inc(full);
           }
         }
-        mbar_cp_async_arrive(full0 + 8 * slot);
+        __syncwarp();
         if (lane == 0) {
           Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
           h->item = more ? item : -1;
@@ -377,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
           h->ng = ng;
           h->rec_cnt = rec_cnt;
           h->fp_cnt = fp_cnt;
-          mbar_arrive(full0 + 8 * slot);
+          mbar_arrive(full);
         }
         k++;
       }

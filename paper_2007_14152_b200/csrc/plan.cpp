@@ -42,6 +42,7 @@ struct spdnn_plan {
   int64_t num_groups = 0;
   int32_t max_fp = 0, max_rec = 0, max_meta = 0;
   int64_t num_fp = 0;
+  int64_t union_records = 0;     // records excluding alignment padding
   int32_t pow2 = 0;              // every nonzero weight is +-2^e (FMA form allowed)
   int32_t wexp_min = 0, wexp_max = 0;
 };
@@ -234,6 +235,10 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
       }
     }
     const int64_t rec_cnt = (int64_t)pl->records.size() / RW - rec_off;
+    pl->union_records += rec_cnt;
+    // keep every stage's records 16-byte aligned for the bulk copy (R = 1
+    // records are 8 bytes): pad with an unreferenced zero record
+    while ((pl->records.size() * 4) % 16) pl->records.push_back(0u);
     pl->max_rec = std::max<int32_t>(pl->max_rec, (int32_t)rec_cnt);
     pl->max_fp = std::max<int32_t>(pl->max_fp, (int32_t)(c_hi - c_lo));
     return std::make_pair(rec_off, rec_cnt);
@@ -405,7 +410,7 @@ extern "C" int spdnn_plan_sizes(const spdnn_plan *pl, spdnn_plan_sizes_t *s) {
   for (size_t b = 0; b < pl->blocks.size(); b += 8) s->num_fp += pl->blocks[b + 5];
   for (size_t st = 0; st < pl->stages.size(); st += 4) s->num_fp += pl->stages[st + 1];
   s->nnz = pl->nnz;
-  s->padded_slots = s->num_records * pl->R;
+  s->padded_slots = pl->union_records * pl->R;
   s->max_fp_per_stage = pl->max_fp;
   s->max_records_per_stage = pl->max_rec;
   s->max_meta_per_block = pl->max_meta;

@@ -107,6 +107,7 @@ class LayerPlan:
     max_meta_per_block: int
     num_records: int
     num_fp: int
+    padded_slots: int
     blocks: np.ndarray    # int32 [num_blocks, 8] descriptors
     stages: np.ndarray    # int32 [num_extra_stages, 4]
     meta: np.ndarray      # int32 per-block fp lists / group segments / rows
@@ -114,7 +115,7 @@ class LayerPlan:
 
     @property
     def total_slots(self) -> int:
-        return self.num_records * self.rows_per_group
+        return self.padded_slots
 
 
 @dataclass(frozen=True)
@@ -151,7 +152,8 @@ def _export(handle) -> LayerPlan:
                      num_blocks=s.num_blocks, max_fp_per_stage=s.max_fp_per_stage,
                      max_records_per_stage=s.max_records_per_stage,
                      max_meta_per_block=s.max_meta_per_block,
-                     num_records=s.num_records, num_fp=s.num_fp, **arrs)
+                     num_records=s.num_records, num_fp=s.num_fp,
+                     padded_slots=s.padded_slots, **arrs)
 
 
 def _padding(layer: LayerCSR, plan: LayerPlan) -> PaddingStats:
