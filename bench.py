@@ -274,6 +274,9 @@ def run_ours(args, cfg):
     layer_ms = np.array([[evs[k][l].elapsed_time(evs[k][l + 1]) for l in range(L)]
                          for k in range(args.steps)])
     counts = ws.counts[: L + 1].cpu().numpy().astype(np.int64)
+    if args.dump_layers and rank == 0:
+        with open(args.dump_layers, "w") as f:
+            json.dump({"counts": counts.tolist(), "layer_ms": layer_ms.mean(axis=0).tolist()}, f)
     ms_step = ms_total / args.steps
     if world > 1:
         t = torch.tensor([ms_step], device=dev)
@@ -365,6 +368,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dump-layers", default="", help="write per-layer counts/times (JSON)")
     ap.add_argument("--cpu-sample", type=int, default=1024,
                     help="inputs in the CPU-baseline sample (0 = skip)")
     args = ap.parse_args()
