@@ -129,6 +129,7 @@ typedef struct spdnn_layer_dev {
   const int32_t *meta;
   const uint32_t *records;
   int64_t num_blocks;
+  int64_t neurons;          /* N: rows of the feature buffers */
   int32_t rows_per_group;
   int32_t record_words;
   int32_t max_fp_per_stage;

@@ -45,8 +45,8 @@ class PlanSizes(ctypes.Structure):
 
 class LayerDev(ctypes.Structure):
     _fields_ = [("blocks", P), ("stages", P), ("meta", P), ("records", P),
-                ("num_blocks", i64), ("rows_per_group", i32), ("record_words", i32),
-                ("max_fp_per_stage", i32), ("max_records_per_stage", i32),
+                ("num_blocks", i64), ("neurons", i64), ("rows_per_group", i32),
+                ("record_words", i32), ("max_fp_per_stage", i32), ("max_records_per_stage", i32),
                 ("max_meta_per_block", i32), ("pad_", i32)]
 
 

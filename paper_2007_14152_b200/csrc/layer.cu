@@ -34,10 +34,15 @@
 //   * the last consumer warp to finish an item publishes its activity bits;
 //     the item that completes tile t appends the tile's alive features to
 //     a_out / cat_out (pruning without a pass over Y).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "common.h"
 
@@ -114,6 +119,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_cp_async_arrive_inc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
+// TMA tile gather: rows r0..r3 of the 2-D tensor, columns [col, col + box),
+// into 4 consecutive smem rows; completion as tx bytes on `bar`
+__device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap *tmap, int col,
+                                            int r0, int r1, int r2, int r3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(sdst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+      "r"(bar)
+      : "memory");
+}
 // TMA bulk copy global -> this CTA's shared memory, completion as tx bytes
 __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32_t bytes,
                                          uint32_t bar) {
@@ -124,6 +140,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32
 }
 
 struct LayerArgs {
+  CUtensorMap tmap_in;  // y_in as a 2-D tensor [N rows][ld cols], box 128 x 1
   spdnn_layer_dev L;
   const float *bias;
   const float *y_in;
@@ -140,6 +157,7 @@ struct LayerArgs {
   int32_t *work;
   uint32_t *guard;     // bit 0: an output in (0, tiny) was produced (FMA form)
   float tiny;
+  uint32_t tiny_bits_m1;  // bits(tiny) - 1: v in (0, tiny) <=> bits(v) - 1 < this
   float negz;          // -0.0f, opaque to the compiler (exact form)
   uint32_t buf_bytes;  // one ring buffer: header | meta | records | y rows
   uint32_t meta_bytes;
@@ -219,52 +237,50 @@ __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int c
 }
 
 // Bias, clamp, store, activity (+ FMA-form guard) for one finished group.
+// rows / bias were loaded before the accumulation (latency hidden).
 template <int R, bool FMA>
 __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, const int *rows,
-                                         int t, int lane, int M, uint32_t *s_alive) {
+                                         const float *bias, int t, int lane, int M,
+                                         uint32_t *s_alive) {
   const int j0 = t * kTile + 4 * lane;
-  bool alive[4] = {false, false, false, false};
-  bool tiny = false;
-  const bool full = j0 + 3 < M;
+  const int valid = M - j0;  // features of this lane that exist (may be <= 0)
+  uint32_t am = 0, tiny = 0;
 #pragma unroll
   for (int k = 0; k < R; k++) {
-    const int row = rows[k];
-    if (row < 0) continue;
-    const float b = __ldg(A.bias + row);
+    if (rows[k] < 0) continue;
+    const u64 b2 = pack2(bias[k], bias[k]);
     float x[4];
-    unpack2(acc[2 * k], x[0], x[1]);
-    unpack2(acc[2 * k + 1], x[2], x[3]);
+    unpack2(add2(acc[2 * k], b2), x[0], x[1]);
+    unpack2(add2(acc[2 * k + 1], b2), x[2], x[3]);
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      x[q] = clamp32(__fadd_rn(x[q], b));
-      alive[q] |= (x[q] > 0.0f);
-      if (FMA) tiny |= (x[q] > 0.0f && x[q] < A.tiny && j0 + q < M);
+      x[q] = clamp32(x[q]);
+      am |= (x[q] > 0.0f) ? (1u << q) : 0u;
+      if (FMA) tiny |= (__float_as_uint(x[q]) - 1u < A.tiny_bits_m1) ? (1u << q) : 0u;
     }
-    float *dst = A.y_out + (int64_t)row * A.ld + j0;
-    if (full) {
+    float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
+    if (valid >= 4) {
       *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
     } else {
 #pragma unroll
       for (int q = 0; q < 4; q++)
-        if (j0 + q < M) dst[q] = x[q];
+        if (q < valid) dst[q] = x[q];
     }
   }
+  const uint32_t vmask = valid >= 4 ? 0xfu : (valid > 0 ? (1u << valid) - 1u : 0u);
+  am &= vmask;
+  if (FMA && (tiny & vmask)) atomicOr(A.guard, 1u);
   // word w of the 128-bit tile mask holds features 32w..32w+31 (lanes 8w..8w+7)
-  uint32_t mine = 0;
-#pragma unroll
-  for (int q = 0; q < 4; q++)
-    if (alive[q] && j0 + q < M) mine |= 1u << q;
-  mine <<= 4 * (lane & 7);
+  const uint32_t mine = am << (4 * (lane & 7));
 #pragma unroll
   for (int w = 0; w < 4; w++) {
     const uint32_t word = __reduce_or_sync(0xffffffffu, (lane >> 3) == w ? mine : 0u);
     if (lane == 0 && word) atomicOr(&s_alive[w], word);
   }
-  if (FMA && tiny) atomicOr(A.guard, 1u);
 }
 
 template <int R, bool FMA>
-__global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) u64 s_full[kBufs], s_empty[kBufs];
   __shared__ uint32_t s_alive[kBufs][4];
@@ -333,7 +349,6 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
       const bool mine_contig = (!ok[0] || src[0] == p0 + 4 * lane) && (!ok[1] || src[1] == p0 + 4 * lane + 1) &&
                                (!ok[2] || src[2] == p0 + 4 * lane + 2) && (!ok[3] || src[3] == p0 + 4 * lane + 3);
       const bool contig = __all_sync(0xffffffffu, mine_contig) && (p0 & 3) == 0;
-      const uint32_t row_bytes = (uint32_t)((valid + 3) & ~3) * 4u;
       for (int s = 0; s < (more ? nst : 1); s++) {
         const int slot = k % kBufs;
         const uint32_t phase = (uint32_t)(k / kBufs) & 1u;
@@ -354,17 +369,28 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
           const int meta_words = s == 0 ? (((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3))
                                         : ((fp_cnt + 3) & ~3);
           const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
+          const int quads = (fp_cnt + 3) >> 2;
           const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
-                              (contig ? (uint32_t)fp_cnt * row_bytes : 0u);
+                              (contig ? (uint32_t)quads * 4u * kRowBytes : 0u);
           if (lane == 0) mbar_expect_tx(full, tx);
           __syncwarp();
           if (lane == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
           if (lane == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
           const int32_t *fp = A.L.meta + meta_off;
           if (contig) {
-            for (int i = lane; i < fp_cnt; i += 32) {
-              const int64_t c = __ldg(fp + i);
-              bulk_g2s(sy + (uint32_t)i * kRowBytes, A.y_in + c * A.ld + p0, row_bytes, full);
+            // 4 staged rows (input neurons) per TMA gather4 of 128 columns
+            for (int qd = lane; qd < quads; qd += 32) {
+              int4 c4;
+              if (4 * qd + 3 < fp_cnt) {
+                c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
+              } else {
+                c4.x = __ldg(fp + 4 * qd);
+                c4.y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : c4.x;
+                c4.z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : c4.x;
+                c4.w = c4.x;
+              }
+              tma_gather4(sy + (uint32_t)qd * 4u * kRowBytes, &A.tmap_in, p0, c4.x, c4.y, c4.z,
+                          c4.w, full);
             }
           } else {
             for (int s0 = 0; s0 < fp_cnt; s0 += 32) {
@@ -404,6 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
   // ======================= consumer warps =======================
   const u64 negz2 = pack2(A.negz, A.negz);
   u64 acc[2 * R];
+  int rows[R];
+  float bias[R];
   for (int k = 0;; k++) {
     const int slot = k % kBufs;
     const uint32_t phase = (uint32_t)(k / kBufs) & 1u;
@@ -416,13 +444,21 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
     const char *ybase = buf + kHeaderBytes + A.meta_bytes + A.rec_bytes + 16 * lane;
     const bool last_stage = h.stage == h.nst - 1;
     if (warp < h.ng) {
+      const int seg_base = (h.fp_cnt + 3) & ~3;
       if (h.stage == 0) {
 #pragma unroll
         for (int r = 0; r < 2 * R; r++) acc[r] = 0ull;
+        // this group's output rows and their biases, fetched ahead of the sums
+        const int *mrows = h.nst == 1 ? meta + seg_base + 2 * h.ng + R * warp
+                                      : meta + seg_base + 2;  // lone multi-stage group
+#pragma unroll
+        for (int r = 0; r < R; r++) {
+          rows[r] = mrows[r];
+          bias[r] = rows[r] >= 0 ? __ldg(A.bias + rows[r]) : 0.0f;
+        }
       }
       int rel, cnt;
-      const int seg_base = (h.fp_cnt + 3) & ~3;
-      if (h.nst == 1 || h.stage == 0) {
+      if (h.stage == 0) {
         rel = meta[seg_base + 2 * warp];
         cnt = meta[seg_base + 2 * warp + 1];
       } else {
@@ -430,24 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(LayerArgs A) {
         cnt = h.rec_cnt;
       }
       accumulate<R, FMA>(acc, recs + (int64_t)rel * RW, cnt, ybase, negz2);
-      if (last_stage) {
-        // rows live in the stage-0 meta; a multi-stage block's last stage
-        // carries only its fp list, so the rows were captured at stage 0
-        if (h.nst == 1) {
-          const int *rows = meta + seg_base + 2 * h.ng + R * warp;
-          epilogue<R, FMA>(A, acc, rows, h.t, lane, M, s_alive[slot]);
-        }
-      }
-    }
-    if (h.nst > 1 && last_stage && warp == 0) {
-      // lone multi-stage group: its rows are re-read from global stage-0 meta
-      const int32_t *blk = A.L.blocks + (int64_t)h.b * 8;
-      const int fp0 = __ldg(blk + 5);
-      const int *rows = A.L.meta + __ldg(blk + 4) + ((fp0 + 3) & ~3) + 2;
-      int rr[R];
-#pragma unroll
-      for (int r = 0; r < R; r++) rr[r] = __ldg(rows + r);
-      epilogue<R, FMA>(A, acc, rr, h.t, lane, M, s_alive[slot]);
+      if (last_stage) epilogue<R, FMA>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
     }
     __syncwarp();
     int bookkeeper = 0;
@@ -545,7 +564,7 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   auto up16 = [](size_t x) { return (x + 15) / 16 * 16; };
   const size_t meta = up16((size_t)L.max_meta_per_block * 4);
   const size_t rec = up16((size_t)L.max_records_per_stage * L.record_words * 4);
-  const size_t ys = (size_t)L.max_fp_per_stage * kRowBytes;
+  const size_t ys = (size_t)((L.max_fp_per_stage + 3) & ~3) * kRowBytes;  // gather4: rows in 4s
   const size_t buf = (kHeaderBytes + meta + rec + ys + 127) / 128 * 128;
   const size_t smem = kBufs * buf;
   if (smem + 2048 > optin)
@@ -620,6 +639,57 @@ __global__ void gather_out_kernel(const float *__restrict__ y, int64_t n, int64_
   }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// y [n][ld] fp32 as a 2-D tensor whose box is one 128-feature row segment:
+// the producer's gather4 fetches 4 such rows (4 input neurons) per TMA op.
+int make_tensor_map(const float *y, int64_t n, int64_t ld, CUtensorMap *out) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return spdnn_fail(SPDNN_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
+  cuuint32_t box[2] = {(cuuint32_t)kTile, 1u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(y), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return spdnn_fail(SPDNN_ECUDA, "cuTensorMapEncodeTiled failed");
+  return SPDNN_OK;
+}
+
+struct TmapCache {
+  std::mutex mu;
+  std::map<std::tuple<const float *, int64_t, int64_t>, CUtensorMap> maps;
+};
+TmapCache g_tmaps;
+
+int tensor_map_for(const float *y, int64_t n, int64_t ld, CUtensorMap *out) {
+  std::lock_guard<std::mutex> lk(g_tmaps.mu);
+  auto key = std::make_tuple(y, n, ld);
+  auto it = g_tmaps.maps.find(key);
+  if (it != g_tmaps.maps.end()) {
+    *out = it->second;
+    return SPDNN_OK;
+  }
+  if (g_tmaps.maps.size() > 64) g_tmaps.maps.clear();
+  int rc = make_tensor_map(y, n, ld, out);
+  if (rc == SPDNN_OK) g_tmaps.maps[key] = *out;
+  return rc;
+}
+
 int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, float *y_out,
             int64_t ld, const int32_t *a_in, const int64_t *cat_in, const int32_t *m_in,
             int32_t *a_out, int64_t *cat_out, int32_t *m_out, const spdnn_scratch *scratch,
@@ -630,7 +700,11 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   const bool fma = opts && opts->fma_form;
   if (fma && !scratch->guard)
     return spdnn_fail(SPDNN_EINVAL, "spdnn_layer_forward: the FMA form needs scratch->guard");
+  if (layer->num_blocks == 0) return SPDNN_OK;  // N == 0
   LayerArgs A;
+  std::memset(&A, 0, sizeof(A));
+  int rc = tensor_map_for(y_in, layer->neurons, ld, &A.tmap_in);
+  if (rc) return rc;
   A.L = *layer;
   A.bias = bias;
   A.y_in = y_in;
@@ -647,9 +721,10 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   A.work = work;
   A.guard = scratch->guard;
   A.tiny = opts ? opts->tiny : 0.0f;
+  uint32_t tb;
+  std::memcpy(&tb, &A.tiny, 4);
+  A.tiny_bits_m1 = tb ? tb - 1u : 0u;
   A.negz = -0.0f;
-  A.buf_bytes = A.meta_bytes = A.rec_bytes = 0;
-  if (A.L.num_blocks == 0) return SPDNN_OK;  // N == 0
   return launch_layer(A, fma, (cudaStream_t)stream);
 }
 

@@ -275,6 +275,7 @@ class DeviceNetwork:
                 buf = self.buffers[k]
                 setattr(d, k, buf.data_ptr() + offsets[k][l] * buf.element_size())
             d.num_blocks = pl.num_blocks
+            d.neurons = pl.neurons
             d.rows_per_group = pl.rows_per_group
             d.record_words = pl.record_words
             d.max_fp_per_stage = pl.max_fp_per_stage
