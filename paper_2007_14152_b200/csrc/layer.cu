@@ -53,7 +53,7 @@ constexpr int kRowBytes = SPDNN_STAGED_ROW_BYTES;
 constexpr int kConsumerWarps = 16;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
 constexpr int kBufs = 2;
-constexpr int kHeaderBytes = 64;
+constexpr int kHeaderBytes = 128;  // keeps every region 128-byte aligned (TMA dst)
 
 typedef unsigned long long u64;
 
@@ -561,9 +561,9 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   int sms;
   size_t optin;
   if (device_info(sms, optin)) return spdnn_fail(SPDNN_ECUDA, "layer: no CUDA device");
-  auto up16 = [](size_t x) { return (x + 15) / 16 * 16; };
-  const size_t meta = up16((size_t)L.max_meta_per_block * 4);
-  const size_t rec = up16((size_t)L.max_records_per_stage * L.record_words * 4);
+  auto up128 = [](size_t x) { return (x + 127) / 128 * 128; };
+  const size_t meta = up128((size_t)L.max_meta_per_block * 4);
+  const size_t rec = up128((size_t)L.max_records_per_stage * L.record_words * 4 + 16);
   const size_t ys = (size_t)((L.max_fp_per_stage + 3) & ~3) * kRowBytes;  // gather4: rows in 4s
   const size_t buf = (kHeaderBytes + meta + rec + ys + 127) / 128 * 128;
   const size_t smem = kBufs * buf;
