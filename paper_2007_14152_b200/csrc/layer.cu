@@ -65,11 +65,15 @@ __device__ __forceinline__ u64 pack2(float a, float b) {
 __device__ __forceinline__ void unpack2(u64 v, float &a, float &b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
 }
-// d = a * w + c per half, one rounding (FFMA2 with a broadcast scalar).
-__device__ __forceinline__ u64 fma2(u64 a, float w, u64 c) {
-  u64 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(pack2(w, w)), "l"(c));
-  return r;
+// acc = y * w + acc in place (the "+l" tie keeps the accumulator register)
+__device__ __forceinline__ void fma2_acc(u64 &acc, u64 y, float w) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(y), "l"(pack2(w, w)));
+}
+// acc = acc + fl(y * w): product rounded first (fma with a -0 addend), exact form
+__device__ __forceinline__ void mul_add2_acc(u64 &acc, u64 y, float w, u64 negz2) {
+  u64 p;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(y), "l"(pack2(w, w)), "l"(negz2));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(p));
 }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) {
   u64 r;
@@ -214,62 +218,100 @@ struct Rec<7> {
 };
 
 // acc[2k], acc[2k+1]: row k, features (4l, 4l+1) and (4l+2, 4l+3).
+// Software-pipelined: record i+2's weights and record i+1's feature values are
+// in flight while record i's 2R FFMA2 issue.
 template <int R, bool FMA>
 __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int cnt,
                                            const char *ybase, u64 negz2) {
-#pragma unroll 2
+  if (cnt <= 0) return;
+  constexpr int RW = Rec<R>::W;
+  uint32_t off0, off1 = 0;
+  float w0[R], w1[R];
+  Rec<R>::load(recs, off0, w0);
+  if (cnt > 1) Rec<R>::load(recs + RW, off1, w1);
+  ulonglong2 y0 = *reinterpret_cast<const ulonglong2 *>(ybase + off0);
   for (int i = 0; i < cnt; i++) {
-    uint32_t off;
-    float w[R];
-    Rec<R>::load(recs + i * Rec<R>::W, off, w);
-    const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ybase + off);
+    // next values (record i+1) and next-next weights (record i+2)
+    ulonglong2 y1 = y0;
+    if (i + 1 < cnt) y1 = *reinterpret_cast<const ulonglong2 *>(ybase + off1);
+    uint32_t off2 = 0;
+    float w2[R];
+    if (i + 2 < cnt) Rec<R>::load(recs + (i + 2) * RW, off2, w2);
 #pragma unroll
     for (int k = 0; k < R; k++) {
       if (FMA) {
-        acc[2 * k] = fma2(y.x, w[k], acc[2 * k]);
-        acc[2 * k + 1] = fma2(y.y, w[k], acc[2 * k + 1]);
+        fma2_acc(acc[2 * k], y0.x, w0[k]);
+        fma2_acc(acc[2 * k + 1], y0.y, w0[k]);
       } else {
-        acc[2 * k] = add2(acc[2 * k], fma2(y.x, w[k], negz2));
-        acc[2 * k + 1] = add2(acc[2 * k + 1], fma2(y.y, w[k], negz2));
+        mul_add2_acc(acc[2 * k], y0.x, w0[k], negz2);
+        mul_add2_acc(acc[2 * k + 1], y0.y, w0[k], negz2);
       }
     }
+    y0 = y1;
+#pragma unroll
+    for (int k = 0; k < R; k++) {
+      w0[k] = w1[k];
+      w1[k] = w2[k];
+    }
+    off1 = off2;
   }
 }
 
 // Bias, clamp, store, activity (+ FMA-form guard) for one finished group.
 // rows / bias were loaded before the accumulation (latency hidden).
+template <int R, bool FMA, bool FULL>
+__device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, const u64 *acc,
+                                                const int *rows, const float *bias, int j0,
+                                                int valid, bool &tiny) {
+  bool a0 = false, a1 = false, a2 = false, a3 = false;
+#pragma unroll
+  for (int k = 0; k < R; k++) {
+    if (rows[k] < 0) continue;
+    const u64 b2 = pack2(bias[k], bias[k]);
+    float x0, x1, x2, x3;
+    unpack2(add2(acc[2 * k], b2), x0, x1);
+    unpack2(add2(acc[2 * k + 1], b2), x2, x3);
+    x0 = clamp32(x0);
+    x1 = clamp32(x1);
+    x2 = clamp32(x2);
+    x3 = clamp32(x3);
+    a0 |= x0 > 0.0f;
+    a1 |= x1 > 0.0f;
+    a2 |= x2 > 0.0f;
+    a3 |= x3 > 0.0f;
+    if (FMA) {
+      const uint32_t tb = A.tiny_bits_m1;
+      tiny |= (__float_as_uint(x0) - 1u < tb) && (FULL || 0 < valid);
+      tiny |= (__float_as_uint(x1) - 1u < tb) && (FULL || 1 < valid);
+      tiny |= (__float_as_uint(x2) - 1u < tb) && (FULL || 2 < valid);
+      tiny |= (__float_as_uint(x3) - 1u < tb) && (FULL || 3 < valid);
+    }
+    float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
+    if (FULL) {
+      *reinterpret_cast<float4 *>(dst) = make_float4(x0, x1, x2, x3);
+    } else {
+      if (0 < valid) dst[0] = x0;
+      if (1 < valid) dst[1] = x1;
+      if (2 < valid) dst[2] = x2;
+      if (3 < valid) dst[3] = x3;
+    }
+  }
+  uint32_t am = (a0 ? 1u : 0u) | (a1 ? 2u : 0u) | (a2 ? 4u : 0u) | (a3 ? 8u : 0u);
+  if (!FULL) am &= valid >= 4 ? 0xfu : (valid > 0 ? (1u << valid) - 1u : 0u);
+  return am;
+}
+
 template <int R, bool FMA>
 __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, const int *rows,
                                          const float *bias, int t, int lane, int M,
                                          uint32_t *s_alive) {
   const int j0 = t * kTile + 4 * lane;
   const int valid = M - j0;  // features of this lane that exist (may be <= 0)
-  uint32_t am = 0, tiny = 0;
-#pragma unroll
-  for (int k = 0; k < R; k++) {
-    if (rows[k] < 0) continue;
-    const u64 b2 = pack2(bias[k], bias[k]);
-    float x[4];
-    unpack2(add2(acc[2 * k], b2), x[0], x[1]);
-    unpack2(add2(acc[2 * k + 1], b2), x[2], x[3]);
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      x[q] = clamp32(x[q]);
-      am |= (x[q] > 0.0f) ? (1u << q) : 0u;
-      if (FMA) tiny |= (__float_as_uint(x[q]) - 1u < A.tiny_bits_m1) ? (1u << q) : 0u;
-    }
-    float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
-    if (valid >= 4) {
-      *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; q++)
-        if (q < valid) dst[q] = x[q];
-    }
-  }
-  const uint32_t vmask = valid >= 4 ? 0xfu : (valid > 0 ? (1u << valid) - 1u : 0u);
-  am &= vmask;
-  if (FMA && (tiny & vmask)) atomicOr(A.guard, 1u);
+  bool tiny = false;
+  const uint32_t am = (t + 1) * kTile <= M
+                          ? finish_rows<R, FMA, true>(A, acc, rows, bias, j0, valid, tiny)
+                          : finish_rows<R, FMA, false>(A, acc, rows, bias, j0, valid, tiny);
+  if (FMA && tiny) atomicOr(A.guard, 1u);
   // word w of the 128-bit tile mask holds features 32w..32w+31 (lanes 8w..8w+7)
   const uint32_t mine = am << (4 * (lane & 7));
 #pragma unroll
@@ -280,7 +322,7 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, con
 }
 
 template <int R, bool FMA>
-__global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constant__ LayerArgs A) {
+__global__ void __maxnreg__(104) layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) u64 s_full[kBufs], s_empty[kBufs];
   __shared__ uint32_t s_alive[kBufs][4];
@@ -335,19 +377,21 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
         rec_off = __shfl_sync(0xffffffffu, v, 6);
         rec_cnt = __shfl_sync(0xffffffffu, v, 7);
       }
-      // this lane's four feature columns of tile t
+      // feature columns 32q + lane (q < 4) of tile t: gathers then write 32
+      // consecutive smem words per instruction (bank-conflict free)
       const int valid = more ? min(kTile, M - t * kTile) : 0;
       int src[4];
       bool ok[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const int f = 4 * lane + q;
+        const int f = 32 * q + lane;
         ok[q] = f < valid;
         src[q] = ok[q] ? __ldg(A.a_in + t * kTile + f) : 0;
       }
       const int p0 = __shfl_sync(0xffffffffu, src[0], 0);
-      const bool mine_contig = (!ok[0] || src[0] == p0 + 4 * lane) && (!ok[1] || src[1] == p0 + 4 * lane + 1) &&
-                               (!ok[2] || src[2] == p0 + 4 * lane + 2) && (!ok[3] || src[3] == p0 + 4 * lane + 3);
+      bool mine_contig = true;
+#pragma unroll
+      for (int q = 0; q < 4; q++) mine_contig &= !ok[q] || src[q] == p0 + 32 * q + lane;
       const bool contig = __all_sync(0xffffffffu, mine_contig) && (p0 & 3) == 0;
       for (int s = 0; s < (more ? nst : 1); s++) {
         const int slot = k % kBufs;
@@ -399,9 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
               for (int i = 0; i < cnt; i++) {
                 const int64_t c = __shfl_sync(0xffffffffu, my, i);
                 const float *row = A.y_in + c * A.ld;
-                const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 16 * lane;
+                const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 4 * lane;
 #pragma unroll
-                for (int q = 0; q < 4; q++) cp_async4(dst + 4 * q, row + src[q], ok[q]);
+                for (int q = 0; q < 4; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
               }
             }
             mbar_cp_async_arrive_inc(full);
