@@ -218,25 +218,24 @@ struct Rec<7> {
 };
 
 // acc[2k], acc[2k+1]: row k, features (4l, 4l+1) and (4l+2, 4l+3).
-// Software-pipelined: record i+2's weights and record i+1's feature values are
-// in flight while record i's 2R FFMA2 issue.
+// Software-pipelined: record i+1 (weights, then its feature values) is loaded
+// while record i's 2R FFMA2 issue.
 template <int R, bool FMA>
 __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int cnt,
                                            const char *ybase, u64 negz2) {
   if (cnt <= 0) return;
   constexpr int RW = Rec<R>::W;
-  uint32_t off0, off1 = 0;
-  float w0[R], w1[R];
-  Rec<R>::load(recs, off0, w0);
-  if (cnt > 1) Rec<R>::load(recs + RW, off1, w1);
-  ulonglong2 y0 = *reinterpret_cast<const ulonglong2 *>(ybase + off0);
+  uint32_t off;
+  float w0[R];
+  Rec<R>::load(recs, off, w0);
+  ulonglong2 y0 = *reinterpret_cast<const ulonglong2 *>(ybase + off);
   for (int i = 0; i < cnt; i++) {
-    // next values (record i+1) and next-next weights (record i+2)
+    float w1[R];
     ulonglong2 y1 = y0;
-    if (i + 1 < cnt) y1 = *reinterpret_cast<const ulonglong2 *>(ybase + off1);
-    uint32_t off2 = 0;
-    float w2[R];
-    if (i + 2 < cnt) Rec<R>::load(recs + (i + 2) * RW, off2, w2);
+    if (i + 1 < cnt) {
+      Rec<R>::load(recs + (i + 1) * RW, off, w1);
+      y1 = *reinterpret_cast<const ulonglong2 *>(ybase + off);
+    }
 #pragma unroll
     for (int k = 0; k < R; k++) {
       if (FMA) {
@@ -249,11 +248,7 @@ __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int c
     }
     y0 = y1;
 #pragma unroll
-    for (int k = 0; k < R; k++) {
-      w0[k] = w1[k];
-      w1[k] = w2[k];
-    }
-    off1 = off2;
+    for (int k = 0; k < R; k++) w0[k] = w1[k];
   }
 }
 
@@ -322,7 +317,7 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, con
 }
 
 template <int R, bool FMA>
-__global__ void __maxnreg__(104) layer_kernel(const __grid_constant__ LayerArgs A) {
+__global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) u64 s_full[kBufs], s_empty[kBufs];
   __shared__ uint32_t s_alive[kBufs][4];
