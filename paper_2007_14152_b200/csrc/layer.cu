@@ -218,37 +218,25 @@ struct Rec<7> {
 };
 
 // acc[2k], acc[2k+1]: row k, features (4l, 4l+1) and (4l+2, 4l+3).
-// Software-pipelined: record i+1 (weights, then its feature values) is loaded
-// while record i's 2R FFMA2 issue.
-template <int R, bool FMA>
+template <int R, bool FMA, int UNROLL>
 __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int cnt,
                                            const char *ybase, u64 negz2) {
-  if (cnt <= 0) return;
-  constexpr int RW = Rec<R>::W;
-  uint32_t off;
-  float w0[R];
-  Rec<R>::load(recs, off, w0);
-  ulonglong2 y0 = *reinterpret_cast<const ulonglong2 *>(ybase + off);
+#pragma unroll UNROLL
   for (int i = 0; i < cnt; i++) {
-    float w1[R];
-    ulonglong2 y1 = y0;
-    if (i + 1 < cnt) {
-      Rec<R>::load(recs + (i + 1) * RW, off, w1);
-      y1 = *reinterpret_cast<const ulonglong2 *>(ybase + off);
-    }
+    uint32_t off;
+    float w[R];
+    Rec<R>::load(recs + i * Rec<R>::W, off, w);
+    const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ybase + off);
 #pragma unroll
     for (int k = 0; k < R; k++) {
       if (FMA) {
-        fma2_acc(acc[2 * k], y0.x, w0[k]);
-        fma2_acc(acc[2 * k + 1], y0.y, w0[k]);
+        fma2_acc(acc[2 * k], y.x, w[k]);
+        fma2_acc(acc[2 * k + 1], y.y, w[k]);
       } else {
-        mul_add2_acc(acc[2 * k], y0.x, w0[k], negz2);
-        mul_add2_acc(acc[2 * k + 1], y0.y, w0[k], negz2);
+        mul_add2_acc(acc[2 * k], y.x, w[k], negz2);
+        mul_add2_acc(acc[2 * k + 1], y.y, w[k], negz2);
       }
     }
-    y0 = y1;
-#pragma unroll
-    for (int k = 0; k < R; k++) w0[k] = w1[k];
   }
 }
 
@@ -504,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
         rel = 0;
         cnt = h.rec_cnt;
       }
-      accumulate<R, FMA>(acc, recs + (int64_t)rel * RW, cnt, ybase, negz2);
+      accumulate<R, FMA, 2>(acc, recs + (int64_t)rel * RW, cnt, ybase, negz2);
       if (last_stage) epilogue<R, FMA>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
     }
     __syncwarp();
