@@ -31,6 +31,7 @@ spdnn/parallel.py): the 60000 inputs are partitioned, weights replicated.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -209,7 +210,9 @@ def run_ours(args, cfg):
     m = shard.active_count
     log(f"[rank {rank}] workload built in {time.time() - t0:.1f}s; preparing {L} layers")
     t0 = time.time()
-    prepared = engine.prepare_model(model, InferenceConfig(), "optimized")
+    params = engine.PlanParams(**{k: int(v) for k, v in
+                                  (kv.split("=") for kv in args.plan.split(",") if kv)})
+    prepared = engine.prepare_model(model, InferenceConfig(), "optimized", params=params)
     net = engine.device_network(prepared, model.bias)
     log(f"[rank {rank}] prepared+uploaded in {time.time() - t0:.1f}s "
         f"({net.hbm_bytes / 1e6:.0f} MB of layout)")
@@ -338,7 +341,8 @@ def run_ours(args, cfg):
                              % (n * ws.ld * 4 / 1e6),
                        "parallelism": f"batch-parallel x{world}" if world > 1 else "single",
                        "arithmetic": "fma form (weights 2^-4, guard clean)" if opts.fma_form
-                                     else "exact form"},
+                                     else "exact form",
+                       "plan": dataclasses.asdict(params)},
             "e2e": {"value": edges_step / e2e_s / 1e12, "unit": "TE/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s * 1e3,
@@ -369,6 +373,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dump-layers", default="", help="write per-layer counts/times (JSON)")
+    ap.add_argument("--plan", default="", help="layout knobs, e.g. max_groups=8,footprint_cap=96")
     ap.add_argument("--cpu-sample", type=int, default=1024,
                     help="inputs in the CPU-baseline sample (0 = skip)")
     args = ap.parse_args()

@@ -83,6 +83,7 @@ typedef struct spdnn_plan_sizes_t {
   int32_t max_fp_per_stage;
   int32_t max_records_per_stage;
   int32_t max_meta_per_block;
+  int32_t max_groups_per_block;
   int32_t pow2;             /* 1: every nonzero weight is +-2^e (FMA form allowed) */
   int32_t wexp_min;         /* exponent range of the nonzero weights */
   int32_t wexp_max;
@@ -135,7 +136,7 @@ typedef struct spdnn_layer_dev {
   int32_t max_fp_per_stage;
   int32_t max_records_per_stage;
   int32_t max_meta_per_block;
-  int32_t pad_;
+  int32_t max_groups_per_block;  /* work units (row groups) per item */
 } spdnn_layer_dev;
 
 /* Per-inference scratch shared by every layer launch (device pointers). */

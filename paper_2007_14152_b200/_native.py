@@ -39,7 +39,8 @@ class PlanSizes(ctypes.Structure):
                 ("num_blocks", i64), ("num_extra_stages", i64), ("num_groups", i64),
                 ("num_meta", i64), ("num_records", i64), ("num_fp", i64), ("nnz", i64),
                 ("padded_slots", i64), ("max_fp_per_stage", i32),
-                ("max_records_per_stage", i32), ("max_meta_per_block", i32), ("pow2", i32),
+                ("max_records_per_stage", i32), ("max_meta_per_block", i32),
+                ("max_groups_per_block", i32), ("pow2", i32),
                 ("wexp_min", i32), ("wexp_max", i32)]
 
 
@@ -47,7 +48,7 @@ class LayerDev(ctypes.Structure):
     _fields_ = [("blocks", P), ("stages", P), ("meta", P), ("records", P),
                 ("num_blocks", i64), ("neurons", i64), ("rows_per_group", i32),
                 ("record_words", i32), ("max_fp_per_stage", i32), ("max_records_per_stage", i32),
-                ("max_meta_per_block", i32), ("pad_", i32)]
+                ("max_meta_per_block", i32), ("max_groups_per_block", i32)]
 
 
 class Scratch(ctypes.Structure):

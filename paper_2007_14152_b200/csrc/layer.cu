@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -52,7 +53,7 @@ constexpr int kTile = SPDNN_TILE_FEATURES;  // 128
 constexpr int kRowBytes = SPDNN_STAGED_ROW_BYTES;
 constexpr int kConsumerWarps = 16;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kBufs = 2;
+constexpr int kMaxBufs = 4;  // ring depth: as many buffers as shared memory holds (<= 4)
 constexpr int kHeaderBytes = 128;  // keeps every region 128-byte aligned (TMA dst)
 
 typedef unsigned long long u64;
@@ -166,6 +167,8 @@ struct LayerArgs {
   uint32_t buf_bytes;  // one ring buffer: header | meta | records | y rows
   uint32_t meta_bytes;
   uint32_t rec_bytes;
+  int nbuf;            // ring depth
+  int gpi;             // consumer work units (row groups) per item = max groups per block
 };
 
 // Ring-buffer header written by the producer (one per buffer fill).
@@ -304,12 +307,56 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, con
   }
 }
 
+// Extra stages of a lone oversized group (rare: a row group whose inputs
+// exceed the staging caps): its records are consumed straight from global
+// memory, the feature values gathered through a_in. Slow, correct.
+template <int R, bool FMA>
+__device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, int lane, int M,
+                                  u64 negz2) {
+  constexpr int RW = Rec<R>::W;
+  const int nst = __ldg(A.L.blocks + (int64_t)b * 8 + 2);
+  const int first_extra = __ldg(A.L.blocks + (int64_t)b * 8 + 3);
+  int pos[4];
+  bool ok[4];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int j = t * kTile + 4 * lane + q;
+    ok[q] = j < M;
+    pos[q] = ok[q] ? __ldg(A.a_in + j) : 0;
+  }
+  for (int s = 1; s < nst; s++) {
+    const int4 sd = __ldg(reinterpret_cast<const int4 *>(A.L.stages) + first_extra + s - 1);
+    const uint32_t *recs = A.L.records + (int64_t)sd.z * RW;
+    for (int i = 0; i < sd.w; i++) {
+      uint32_t off;
+      float w[R];
+      Rec<R>::load(recs + i * RW, off, w);  // (global loads)
+      const int64_t c = __ldg(A.L.meta + sd.x + off / kRowBytes);
+      const float *row = A.y_in + c * A.ld;
+      float v[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) v[q] = ok[q] ? __ldg(row + pos[q]) : 0.0f;
+      const u64 y01 = pack2(v[0], v[1]), y23 = pack2(v[2], v[3]);
+#pragma unroll
+      for (int k = 0; k < R; k++) {
+        if (FMA) {
+          fma2_acc(acc[2 * k], y01, w[k]);
+          fma2_acc(acc[2 * k + 1], y23, w[k]);
+        } else {
+          mul_add2_acc(acc[2 * k], y01, w[k], negz2);
+          mul_add2_acc(acc[2 * k + 1], y23, w[k], negz2);
+        }
+      }
+    }
+  }
+}
+
 template <int R, bool FMA>
 __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(8) u64 s_full[kBufs], s_empty[kBufs];
-  __shared__ uint32_t s_alive[kBufs][4];
-  __shared__ int s_done[kBufs];
+  __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
+  __shared__ uint32_t s_alive[kMaxBufs][4];
+  __shared__ int s_done[kMaxBufs];
 
   constexpr int RW = Rec<R>::W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -318,14 +365,15 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   const int nb = (int)A.L.num_blocks;
   const int tiles = (M + kTile - 1) / kTile;
   const int items = tiles * nb;
+  const int nbuf = A.nbuf, gpi = A.gpi;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
   const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(&s_empty[0]);
 
   if (tid == 0) {
-    for (int i = 0; i < kBufs; i++) {
-      mbar_init(full0 + 8 * i, 1);                 // the header arrival (+ tx bytes)
-      mbar_init(empty0 + 8 * i, kConsumerWarps);  // one per consumer warp
+    for (int i = 0; i < nbuf; i++) {
+      mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
+      mbar_init(empty0 + 8 * i, gpi);  // one arrival per work unit (row group) of the item
       s_done[i] = 0;
       for (int w = 0; w < 4; w++) s_alive[i][w] = 0u;
     }
@@ -335,18 +383,18 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
 
   if (warp == kConsumerWarps) {
     // ======================= producer warp =======================
-    // Per ring fill: TMA bulk copies for the block metadata, the union
-    // records and -- when the tile's 128 feature columns are contiguous (the
-    // steady state; every tile right after a death-free layer) -- one 512-byte
-    // row per staged input neuron. Tiles holding gaps left by features that
-    // died in the previous layer are gathered with 4-byte cp.async instead.
-    int k = 0;
-    for (;;) {
+    // Per item (= ring fill): TMA bulk copies of the block's metadata and
+    // union records and -- when the tile's 128 feature columns are contiguous
+    // (the steady state: every tile after a layer without deaths) -- TMA
+    // gather4 of the staged rows, 4 input neurons x 512 bytes per op. Tiles
+    // with gaps left by features that died in the previous layer are
+    // gathered with 4-byte cp.async instead.
+    for (int k = 0;; k++) {
       int item = 0;
       if (lane == 0) item = atomicAdd(A.work, 1);
       item = __shfl_sync(0xffffffffu, item, 0);
       const bool more = item < items;
-      int t = 0, b = 0, ng = 0, nst = 1, first_extra = 0;
+      int t = 0, b = 0, ng = 0, nst = 1;
       int meta_off = 0, fp_cnt = 0, rec_off = 0, rec_cnt = 0;
       if (more) {
         t = item / nb;
@@ -354,7 +402,6 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
         const int v = lane < 8 ? __ldg(A.L.blocks + (int64_t)b * 8 + lane) : 0;
         ng = __shfl_sync(0xffffffffu, v, 1);
         nst = __shfl_sync(0xffffffffu, v, 2);
-        first_extra = __shfl_sync(0xffffffffu, v, 3);
         meta_off = __shfl_sync(0xffffffffu, v, 4);
         fp_cnt = __shfl_sync(0xffffffffu, v, 5);
         rec_off = __shfl_sync(0xffffffffu, v, 6);
@@ -376,78 +423,67 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
 #pragma unroll
       for (int q = 0; q < 4; q++) mine_contig &= !ok[q] || src[q] == p0 + 32 * q + lane;
       const bool contig = __all_sync(0xffffffffu, mine_contig) && (p0 & 3) == 0;
-      for (int s = 0; s < (more ? nst : 1); s++) {
-        const int slot = k % kBufs;
-        const uint32_t phase = (uint32_t)(k / kBufs) & 1u;
-        if (s > 0) {
-          const int4 sd = __ldg(reinterpret_cast<const int4 *>(A.L.stages) + first_extra + s - 1);
-          meta_off = sd.x;
-          fp_cnt = sd.y;
-          rec_off = sd.z;
-          rec_cnt = sd.w;
-        }
-        mbar_wait(empty0 + 8 * slot, phase ^ 1u);
-        const uint32_t full = full0 + 8 * slot;
-        const uint32_t buf = sbase + slot * A.buf_bytes;
-        const uint32_t smeta = buf + kHeaderBytes;
-        const uint32_t srec = smeta + A.meta_bytes;
-        const uint32_t sy = srec + A.rec_bytes;
-        if (more) {
-          const int meta_words = s == 0 ? (((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3))
-                                        : ((fp_cnt + 3) & ~3);
-          const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
-          const int quads = (fp_cnt + 3) >> 2;
-          const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
-                              (contig ? (uint32_t)quads * 4u * kRowBytes : 0u);
-          if (lane == 0) mbar_expect_tx(full, tx);
-          __syncwarp();
-          if (lane == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
-          if (lane == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
-          const int32_t *fp = A.L.meta + meta_off;
-          if (contig) {
-            // 4 staged rows (input neurons) per TMA gather4 of 128 columns
-            for (int qd = lane; qd < quads; qd += 32) {
-              int4 c4;
-              if (4 * qd + 3 < fp_cnt) {
-                c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
-              } else {
-                c4.x = __ldg(fp + 4 * qd);
-                c4.y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : c4.x;
-                c4.z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : c4.x;
-                c4.w = c4.x;
-              }
-              tma_gather4(sy + (uint32_t)qd * 4u * kRowBytes, &A.tmap_in, p0, c4.x, c4.y, c4.z,
-                          c4.w, full);
-            }
-          } else {
-            for (int s0 = 0; s0 < fp_cnt; s0 += 32) {
-              const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
-              const int cnt = min(32, fp_cnt - s0);
-              for (int i = 0; i < cnt; i++) {
-                const int64_t c = __shfl_sync(0xffffffffu, my, i);
-                const float *row = A.y_in + c * A.ld;
-                const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 4 * lane;
-#pragma unroll
-                for (int q = 0; q < 4; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
-              }
-            }
-            mbar_cp_async_arrive_inc(full);
-          }
-        }
+
+      const int slot = k % nbuf;
+      const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
+      mbar_wait(empty0 + 8 * slot, phase ^ 1u);
+      const uint32_t full = full0 + 8 * slot;
+      const uint32_t buf = sbase + slot * A.buf_bytes;
+      const uint32_t smeta = buf + kHeaderBytes;
+      const uint32_t srec = smeta + A.meta_bytes;
+      const uint32_t sy = srec + A.rec_bytes;
+      if (more) {
+        const int meta_words = ((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3);
+        const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
+        const int quads = (fp_cnt + 3) >> 2;
+        const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
+                            (contig ? (uint32_t)quads * 4u * kRowBytes : 0u);
+        if (lane == 0) mbar_expect_tx(full, tx);
         __syncwarp();
-        if (lane == 0) {
-          Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
-          h->item = more ? item : -1;
-          h->t = t;
-          h->b = b;
-          h->stage = s;
-          h->nst = nst;
-          h->ng = ng;
-          h->rec_cnt = rec_cnt;
-          h->fp_cnt = fp_cnt;
-          mbar_arrive(full);
+        if (lane == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
+        if (lane == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
+        const int32_t *fp = A.L.meta + meta_off;
+        if (contig) {
+          for (int qd = lane; qd < quads; qd += 32) {
+            int4 c4;
+            if (4 * qd + 3 < fp_cnt) {
+              c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
+            } else {
+              c4.x = __ldg(fp + 4 * qd);
+              c4.y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : c4.x;
+              c4.z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : c4.x;
+              c4.w = c4.x;
+            }
+            tma_gather4(sy + (uint32_t)qd * 4u * kRowBytes, &A.tmap_in, p0, c4.x, c4.y, c4.z,
+                        c4.w, full);
+          }
+        } else {
+          for (int s0 = 0; s0 < fp_cnt; s0 += 32) {
+            const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
+            const int cnt = min(32, fp_cnt - s0);
+            for (int i = 0; i < cnt; i++) {
+              const int64_t c = __shfl_sync(0xffffffffu, my, i);
+              const float *row = A.y_in + c * A.ld;
+              const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 4 * lane;
+#pragma unroll
+              for (int q = 0; q < 4; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
+            }
+          }
+          mbar_cp_async_arrive_inc(full);
         }
-        k++;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
+        h->item = more ? item : -1;
+        h->t = t;
+        h->b = b;
+        h->stage = 0;
+        h->nst = nst;
+        h->ng = ng;
+        h->rec_cnt = rec_cnt;
+        h->fp_cnt = fp_cnt;
+        mbar_arrive(full);
       }
       if (!more) break;
     }
@@ -455,57 +491,48 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   }
 
   // ======================= consumer warps =======================
+  // Work unit u = (item k = u / gpi, row group g = u % gpi); warp w takes
+  // units w, w + 16, ... so all warps stay busy whatever the group count per
+  // item, and items overlap in the ring.
   const u64 negz2 = pack2(A.negz, A.negz);
-  u64 acc[2 * R];
-  int rows[R];
-  float bias[R];
-  for (int k = 0;; k++) {
-    const int slot = k % kBufs;
-    const uint32_t phase = (uint32_t)(k / kBufs) & 1u;
+  for (int u = warp;; u += kConsumerWarps) {
+    const int k = u / gpi, g = u - k * gpi;
+    const int slot = k % nbuf;
+    const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
     mbar_wait(full0 + 8 * slot, phase);
     const char *buf = smem + slot * A.buf_bytes;
     const Header h = *reinterpret_cast<const Header *>(buf);
     if (h.item < 0) break;
-    const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
-    const uint32_t *recs = reinterpret_cast<const uint32_t *>(buf + kHeaderBytes + A.meta_bytes);
-    const char *ybase = buf + kHeaderBytes + A.meta_bytes + A.rec_bytes + 16 * lane;
-    const bool last_stage = h.stage == h.nst - 1;
-    if (warp < h.ng) {
+    if (g < h.ng) {
+      const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
+      const uint32_t *recs = reinterpret_cast<const uint32_t *>(buf + kHeaderBytes + A.meta_bytes);
+      const char *ybase = buf + kHeaderBytes + A.meta_bytes + A.rec_bytes + 16 * lane;
       const int seg_base = (h.fp_cnt + 3) & ~3;
-      if (h.stage == 0) {
+      int rows[R];
+      float bias[R];
+      const int *mrows = meta + seg_base + 2 * h.ng + R * g;
 #pragma unroll
-        for (int r = 0; r < 2 * R; r++) acc[r] = 0ull;
-        // this group's output rows and their biases, fetched ahead of the sums
-        const int *mrows = h.nst == 1 ? meta + seg_base + 2 * h.ng + R * warp
-                                      : meta + seg_base + 2;  // lone multi-stage group
+      for (int r = 0; r < R; r++) {
+        rows[r] = mrows[r];
+        bias[r] = rows[r] >= 0 ? __ldg(A.bias + rows[r]) : 0.0f;
+      }
+      u64 acc[2 * R];
 #pragma unroll
-        for (int r = 0; r < R; r++) {
-          rows[r] = mrows[r];
-          bias[r] = rows[r] >= 0 ? __ldg(A.bias + rows[r]) : 0.0f;
-        }
-      }
-      int rel, cnt;
-      if (h.stage == 0) {
-        rel = meta[seg_base + 2 * warp];
-        cnt = meta[seg_base + 2 * warp + 1];
-      } else {
-        rel = 0;
-        cnt = h.rec_cnt;
-      }
-      accumulate<R, FMA, 2>(acc, recs + (int64_t)rel * RW, cnt, ybase, negz2);
-      if (last_stage) epilogue<R, FMA>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
+      for (int r = 0; r < 2 * R; r++) acc[r] = 0ull;
+      accumulate<R, FMA, 2>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
+                            meta[seg_base + 2 * g + 1], ybase, negz2);
+      if (h.nst > 1) accumulate_global<R, FMA>(A, acc, h.b, h.t, lane, M, negz2);
+      epilogue<R, FMA>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
     }
     __syncwarp();
     int bookkeeper = 0;
-    if (last_stage) {
-      if (lane == 0) {
-        __threadfence_block();
-        bookkeeper = atomicAdd(&s_done[slot], 1) == kConsumerWarps - 1;
-      }
-      bookkeeper = __shfl_sync(0xffffffffu, bookkeeper, 0);
+    if (lane == 0) {
+      __threadfence_block();
+      bookkeeper = atomicAdd(&s_done[slot], 1) == gpi - 1;
     }
+    bookkeeper = __shfl_sync(0xffffffffu, bookkeeper, 0);
     if (bookkeeper) {
-      // every consumer warp has published its activity bits for this item
+      // every unit of the item has published its activity bits
       __threadfence_block();
       uint32_t w4 = lane < 4 ? s_alive[slot][lane] : 0u;
       __syncwarp();
@@ -593,12 +620,15 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   const size_t rec = up128((size_t)L.max_records_per_stage * L.record_words * 4 + 16);
   const size_t ys = (size_t)((L.max_fp_per_stage + 3) & ~3) * kRowBytes;  // gather4: rows in 4s
   const size_t buf = (kHeaderBytes + meta + rec + ys + 127) / 128 * 128;
-  const size_t smem = kBufs * buf;
-  if (smem + 2048 > optin)
-    return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
+  const size_t budget = optin - 2048;  // static shared memory + reserve
+  const int nbuf = (int)std::min<size_t>(kMaxBufs, budget / buf);
+  if (nbuf < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
+  const size_t smem = (size_t)nbuf * buf;
   A.meta_bytes = (uint32_t)meta;
   A.rec_bytes = (uint32_t)rec;
   A.buf_bytes = (uint32_t)buf;
+  A.nbuf = nbuf;
+  A.gpi = std::max(1, L.max_groups_per_block);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   int per_sm = 0;

@@ -40,7 +40,7 @@ struct spdnn_plan {
   std::vector<uint32_t> records;
   int64_t nnz = 0;
   int64_t num_groups = 0;
-  int32_t max_fp = 0, max_rec = 0, max_meta = 0;
+  int32_t max_fp = 0, max_rec = 0, max_meta = 0, max_groups = 0;
   int64_t num_fp = 0;
   int64_t union_records = 0;     // records excluding alignment padding
   int32_t pow2 = 0;              // every nonzero weight is +-2^e (FMA form allowed)
@@ -263,6 +263,7 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
       g++;
     }
     const size_t ng = g - g0;
+    pl->max_groups = std::max<int32_t>(pl->max_groups, (int32_t)ng);
     std::sort(fp_block.begin(), fp_block.end());
     const int64_t nfp = (int64_t)fp_block.size();
     // a block overflows the caps only when it is a lone group (loop above)
@@ -414,6 +415,7 @@ extern "C" int spdnn_plan_sizes(const spdnn_plan *pl, spdnn_plan_sizes_t *s) {
   s->max_fp_per_stage = pl->max_fp;
   s->max_records_per_stage = pl->max_rec;
   s->max_meta_per_block = pl->max_meta;
+  s->max_groups_per_block = pl->max_groups;
   s->pow2 = pl->pow2;
   s->wexp_min = pl->wexp_min;
   s->wexp_max = pl->wexp_max;

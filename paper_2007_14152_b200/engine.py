@@ -105,6 +105,7 @@ class LayerPlan:
     max_fp_per_stage: int
     max_records_per_stage: int
     max_meta_per_block: int
+    max_groups_per_block: int
     num_records: int
     num_fp: int
     padded_slots: int
@@ -152,6 +153,7 @@ def _export(handle) -> LayerPlan:
                      num_blocks=s.num_blocks, max_fp_per_stage=s.max_fp_per_stage,
                      max_records_per_stage=s.max_records_per_stage,
                      max_meta_per_block=s.max_meta_per_block,
+                     max_groups_per_block=s.max_groups_per_block,
                      num_records=s.num_records, num_fp=s.num_fp,
                      padded_slots=s.padded_slots, **arrs)
 
@@ -281,6 +283,8 @@ class DeviceNetwork:
             d.max_fp_per_stage = pl.max_fp_per_stage
             d.max_records_per_stage = pl.max_records_per_stage
             d.max_meta_per_block = pl.max_meta_per_block
+            # one launch serves all layers' items with the same unit count
+            d.max_groups_per_block = pl.max_groups_per_block
         # FMA form (one FFMA2 per (row, column)) is exact when every weight is
         # +-2^e and no input falls below `tiny` (products stay normal) or above
         # `huge` (no overflow); the kernels flag violations and infer() reruns
