@@ -102,6 +102,20 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar)
                : "memory");
 }
+// One bounded wait (suspends up to ~2 us): true when the phase with `parity` is done.
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(2000)
+      : "memory");
+  return ok != 0;
+}
 // Blocks (suspended, up to the time hint) until the phase with `parity` is done.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
@@ -357,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ int s_done[kMaxBufs];
+  __shared__ int s_end;  // ring entries the producer will fill (set when work runs out)
 
   constexpr int RW = Rec<R>::W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -377,6 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       s_done[i] = 0;
       for (int w = 0; w < 4; w++) s_alive[i][w] = 0u;
     }
+    s_end = 0x7fffffff;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -393,7 +409,12 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       int item = 0;
       if (lane == 0) item = atomicAdd(A.work, 1);
       item = __shfl_sync(0xffffffffu, item, 0);
-      const bool more = item < items;
+      if (item >= items) {
+        // no more work: consumers waiting on entries >= k leave
+        if (lane == 0) atomicExch(&s_end, k);
+        break;
+      }
+      const bool more = true;
       int t = 0, b = 0, ng = 0, nst = 1;
       int meta_off = 0, fp_cnt = 0, rec_off = 0, rec_cnt = 0;
       if (more) {
@@ -485,7 +506,6 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
         h->fp_cnt = fp_cnt;
         mbar_arrive(full);
       }
-      if (!more) break;
     }
     return;
   }
@@ -499,10 +519,16 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
     const int k = u / gpi, g = u - k * gpi;
     const int slot = k % nbuf;
     const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
-    mbar_wait(full0 + 8 * slot, phase);
+    bool done = false;
+    while (!mbar_try_wait(full0 + 8 * slot, phase)) {
+      if (k >= *reinterpret_cast<volatile int *>(&s_end)) {
+        done = true;
+        break;
+      }
+    }
+    if (done) break;
     const char *buf = smem + slot * A.buf_bytes;
     const Header h = *reinterpret_cast<const Header *>(buf);
-    if (h.item < 0) break;
     if (g < h.ng) {
       const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
       const uint32_t *recs = reinterpret_cast<const uint32_t *>(buf + kHeaderBytes + A.meta_bytes);
@@ -621,14 +647,23 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   const size_t ys = (size_t)((L.max_fp_per_stage + 3) & ~3) * kRowBytes;  // gather4: rows in 4s
   const size_t buf = (kHeaderBytes + meta + rec + ys + 127) / 128 * 128;
   const size_t budget = optin - 2048;  // static shared memory + reserve
-  const int nbuf = (int)std::min<size_t>(kMaxBufs, budget / buf);
+  // Ring depth and units per item. Consumer warp w visits every (16/gpi)-th
+  // ring entry; with nbuf a multiple of 16/gpi it has itself consumed entry
+  // k - nbuf before it waits on entry k, so an mbarrier phase can never be
+  // mistaken for the one nbuf entries earlier.
+  int nbuf = (int)std::min<size_t>(kMaxBufs, budget / buf);
+  if (nbuf == 3) nbuf = 2;
   if (nbuf < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
+  int gpi = 1;
+  while (gpi < L.max_groups_per_block) gpi *= 2;
+  gpi = std::max(gpi, kConsumerWarps / nbuf);
+  if (gpi > kConsumerWarps) return spdnn_fail(SPDNN_EINVAL, "layer: more row groups per block than warps");
   const size_t smem = (size_t)nbuf * buf;
   A.meta_bytes = (uint32_t)meta;
   A.rec_bytes = (uint32_t)rec;
   A.buf_bytes = (uint32_t)buf;
   A.nbuf = nbuf;
-  A.gpi = std::max(1, L.max_groups_per_block);
+  A.gpi = gpi;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   int per_sm = 0;
