@@ -371,7 +371,6 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ int s_done[kMaxBufs];
-  __shared__ int s_end;  // ring entries the producer will fill (set when work runs out)
 
   constexpr int RW = Rec<R>::W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -392,7 +391,6 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       s_done[i] = 0;
       for (int w = 0; w < 4; w++) s_alive[i][w] = 0u;
     }
-    s_end = 0x7fffffff;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -410,8 +408,17 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       if (lane == 0) item = atomicAdd(A.work, 1);
       item = __shfl_sync(0xffffffffu, item, 0);
       if (item >= items) {
-        // no more work: consumers waiting on entries >= k leave
-        if (lane == 0) atomicExch(&s_end, k);
+        // no more work: end markers in the next nbuf entries. A consumer warp
+        // waits at most 16/gpi <= nbuf entries past the last one it served.
+        for (int e = 0; e < nbuf; e++, k++) {
+          const int slot = k % nbuf;
+          mbar_wait(empty0 + 8 * slot, ((uint32_t)(k / nbuf) & 1u) ^ 1u);
+          if (lane == 0) {
+            reinterpret_cast<Header *>(smem + slot * A.buf_bytes)->item = -1;
+            mbar_arrive(full0 + 8 * slot);
+          }
+          __syncwarp();
+        }
         break;
       }
       const bool more = true;
@@ -519,16 +526,10 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
     const int k = u / gpi, g = u - k * gpi;
     const int slot = k % nbuf;
     const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
-    bool done = false;
-    while (!mbar_try_wait(full0 + 8 * slot, phase)) {
-      if (k >= *reinterpret_cast<volatile int *>(&s_end)) {
-        done = true;
-        break;
-      }
-    }
-    if (done) break;
+    mbar_wait(full0 + 8 * slot, phase);
     const char *buf = smem + slot * A.buf_bytes;
     const Header h = *reinterpret_cast<const Header *>(buf);
+    if (h.item < 0) break;
     if (g < h.ng) {
       const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
       const uint32_t *recs = reinterpret_cast<const uint32_t *>(buf + kHeaderBytes + A.meta_bytes);
@@ -566,12 +567,19 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       if (lane == 0) s_done[slot] = 0;
       int last = 0;
       if (lane < 4 && w4) atomicOr(&A.tile_alive[4 * h.t + lane], w4);
-      __threadfence();
       __syncwarp();
-      if (lane == 0) last = atomicAdd(&A.tile_done[h.t], 1) == nb - 1;
+      if (lane == 0) {
+        // release: our tile_alive bits before the count; the last arrival
+        // acquires everyone's (acq_rel instead of a full __threadfence)
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n"
+                     : "=r"(old)
+                     : "l"(A.tile_done + h.t)
+                     : "memory");
+        last = old == nb - 1;
+      }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        __threadfence();
         if (lane < 4) {
           w4 = atomicOr(&A.tile_alive[4 * h.t + lane], 0u);
           A.tile_alive[4 * h.t + lane] = 0u;
