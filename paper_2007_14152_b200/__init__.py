@@ -13,5 +13,8 @@ from .ingest import GeneratorSpec, generate_synthetic_inputs, generate_synthetic
 from .engine import (InferenceResult, LayerOutcome, LayerPlan, PaddingStats, PlanParams,
                      PreparedLayer, baseline_layer, compact_active, infer, optimized_layer,
                      prepare_model, run_layer_step)
+from .parallel import (BalanceEntry, BalanceReport, CommMatrix, CountMsg, GatherMsg, Partition,
+                       RowsMsg, apply_transfers, balance_step, gather_categories,
+                       imbalance_ratio, partition_even, run_batch_parallel)
 
 __version__ = "0.1.0"

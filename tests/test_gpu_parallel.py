@@ -1,0 +1,106 @@
+"""GPU batch-parallel runner (parallel.run_batch_parallel, in-process workers
+on one device): the reference's parallel test cases (tests/test_parallel.py
+of the reference) against the single-worker engine and the oracle."""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle
+from paper_2007_14152_b200 import engine, ingest, parallel
+from paper_2007_14152_b200.model import InferenceConfig, ModelError, make_feature_batch
+
+pytestmark = pytest.mark.gpu
+
+
+def _small(density=0.8, m=40):
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=64, layers=5, connections_per_neuron=16, bias_value=0.0625, seed=31))
+    return model, ingest.generate_synthetic_inputs(64, m, density, seed=32)
+
+
+def _edge(m=400):
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=12, connections_per_neuron=32, bias_value=-0.3, seed=1))
+    return model, ingest.generate_synthetic_inputs(1024, m, 0.3, seed=2)
+
+
+def _check_same(res, single):
+    assert np.array_equal(res.categories, single.categories)
+    assert np.array_equal(np.asarray(res.final.data).view(np.uint32),
+                          np.asarray(single.final.data).view(np.uint32))
+    for a, b in zip(res.per_layer, single.per_layer):
+        assert (a.active_before, a.active_after) == (b.active_before, b.active_after)
+
+
+@pytest.mark.parametrize("workers", [1, 2, 3, 5, 8])
+def test_worker_count_invariance(cuda_ok, workers):
+    for model, inputs in (_small(), _edge()):
+        cfg = InferenceConfig(workers=workers, rebalance_threshold=1.1)
+        res, comm, bal = parallel.run_batch_parallel(model, inputs, cfg)
+        _check_same(res, engine.infer(model, inputs, cfg))
+        assert np.trace(comm.matrix) == 0 and comm.total_moved == bal.total_moved
+
+
+def test_adversarial_die_off_triggers_rebalance(cuda_ok):
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=64, layers=4, connections_per_neuron=32, bias_value=-0.3, seed=3))
+    data = np.ones((64, 60), dtype=np.float32)
+    data[:, 30:] = 0.0
+    inputs = make_feature_batch(64, data)
+    res, comm, bal = parallel.run_batch_parallel(model, inputs, InferenceConfig(workers=2))
+    _check_same(res, engine.infer(model, inputs, InferenceConfig()))
+    assert res.categories.tolist() == oracle.infer(model, inputs).categories.tolist()
+    reb = [e for e in bal.entries if e.rebalanced]
+    assert reb and all(max(e.after_counts) - min(e.after_counts) <= 1 for e in reb)
+    assert comm.matrix[0, 1] == reb[0].moved_rows
+    res2, comm2, bal2 = parallel.run_batch_parallel(
+        model, inputs, InferenceConfig(workers=2, rebalance_threshold=math.inf))
+    assert np.array_equal(res2.categories, res.categories)
+    assert not comm2.matrix.any() and not any(e.rebalanced for e in bal2.entries)
+
+
+def test_skewed_stress_rebalancing(cuda_ok):
+    """SURVEY.md 8(d) C5 recipe at small scale: per-shard densities skewed."""
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=24, connections_per_neuron=32, bias_value=-0.3, seed=1))
+    parts = [ingest.generate_synthetic_inputs(1024, 300, 0.34 - 0.01 * s, seed=100 + s)
+             for s in range(8)]
+    inputs = make_feature_batch(1024, np.concatenate([p.data for p in parts], axis=1))
+    ref = oracle.infer(model, inputs, threads=8)
+    on = parallel.run_batch_parallel(model, inputs, InferenceConfig(workers=8))
+    off = parallel.run_batch_parallel(model, inputs,
+                                      InferenceConfig(workers=8, rebalance_threshold=math.inf))
+    for res, comm, bal in (on, off):
+        assert res.categories.tolist() == ref.categories.tolist()
+    assert on[1].total_moved > 0 and off[1].total_moved == 0
+    worst_on = max(e.imbalance_after for e in on[2].entries if e.before_counts[0] >= 0)
+    assert worst_on <= 1.25 or any(e.rebalanced for e in on[2].entries)
+
+
+def test_latency_hook_sees_typed_messages(cuda_ok):
+    model, inputs = _small(m=30)
+    seen = []
+    cfg = InferenceConfig(workers=3, rebalance_threshold=1.05)
+    res, _, _ = parallel.run_batch_parallel(model, inputs, cfg, latency_hook=seen.append)
+    assert np.array_equal(res.categories, engine.infer(model, inputs, cfg).categories)
+    assert parallel.CountMsg in {type(m) for m in seen}
+
+
+def test_baseline_mode_and_more_workers_than_features(cuda_ok):
+    model, inputs = _small(m=24)
+    cfg = InferenceConfig(workers=3)
+    res, _, _ = parallel.run_batch_parallel(model, inputs, cfg, mode="baseline")
+    _check_same(res, engine.infer(model, inputs, cfg, mode="baseline"))
+    model, inputs = _small(m=3)
+    res, _, _ = parallel.run_batch_parallel(model, inputs, InferenceConfig(workers=6))
+    assert np.array_equal(res.categories, engine.infer(model, inputs, InferenceConfig()).categories)
+
+
+def test_wrong_mode_prepared_raises(cuda_ok):
+    model, inputs = _small(m=12)
+    cfg = InferenceConfig(workers=2)
+    bad = engine.prepare_model(model, cfg, "baseline")
+    with pytest.raises(ModelError):
+        parallel.run_batch_parallel(model, inputs, cfg, mode="optimized", prepared=bad)
