@@ -401,11 +401,22 @@ class DistTransport:
         self.root = self.rank == 0
         self.hook = hook
         self.device = device
+        # NCCL moves device tensors; gloo (CPU tests, or several ranks sharing
+        # one GPU) moves host copies
+        self.wire = device if dist.get_backend() == "nccl" else None
+
+    def _wire(self, t):
+        return t if self.wire is not None else t.cpu()
+
+    def _empty(self, shape, dtype):
+        import torch
+        return torch.empty(shape, dtype=dtype,
+                           device=self.device if self.wire is not None else "cpu")
 
     def allgather_counts(self, layer: int, mine: dict) -> list:
         import torch
-        t = torch.tensor([mine[self.rank]], dtype=torch.int64, device=self.device)
-        out = [torch.empty(1, dtype=torch.int64, device=self.device) for _ in range(self.workers)]
+        t = self._wire(torch.tensor([mine[self.rank]], dtype=torch.int64, device=self.device))
+        out = [self._empty(1, torch.int64) for _ in range(self.workers)]
         self.dist.all_gather(out, t)  # NCCL allgather on GPUs (gloo on CPU)
         if self.hook is not None:
             for other in range(self.workers):
@@ -424,11 +435,11 @@ class DistTransport:
                 vals, cats = me.take_top(k)
                 if self.hook is not None:
                     self.hook(RowsMsg(src=src, dst=dst, layer=layer, data=vals, categories=cats))
-                ops.append(self.dist.P2POp(self.dist.isend, vals.contiguous(), dst))
-                ops.append(self.dist.P2POp(self.dist.isend, cats.contiguous(), dst))
+                ops.append(self.dist.P2POp(self.dist.isend, self._wire(vals.contiguous()), dst))
+                ops.append(self.dist.P2POp(self.dist.isend, self._wire(cats.contiguous()), dst))
             elif dst == self.rank:
-                vals = torch.empty((k, me.n), dtype=torch.float32, device=self.device)
-                cats = torch.empty(k, dtype=torch.int64, device=self.device)
+                vals = self._empty((k, me.n), torch.float32)
+                cats = self._empty(k, torch.int64)
                 ops.append(self.dist.P2POp(self.dist.irecv, vals, src))
                 ops.append(self.dist.P2POp(self.dist.irecv, cats, src))
                 recv.append((vals, cats))
@@ -446,13 +457,12 @@ class DistTransport:
         n = shards[self.rank].n
         parts = []
         for w in range(self.workers):
-            c = cats if w == self.rank else torch.empty(counts[w], dtype=torch.int64,
-                                                        device=self.device)
+            c = self._wire(cats) if w == self.rank else self._empty(counts[w], torch.int64)
             self.dist.broadcast(c, src=w)
             v = None
             if values:
-                v = vals if w == self.rank else torch.empty((counts[w], n), dtype=torch.float32,
-                                                            device=self.device)
+                v = self._wire(vals) if w == self.rank else self._empty((counts[w], n),
+                                                                         torch.float32)
                 self.dist.broadcast(v, src=w)
             parts.append((c, v))
         return parts

@@ -104,3 +104,53 @@ def test_wrong_mode_prepared_raises(cuda_ok):
     bad = engine.prepare_model(model, cfg, "baseline")
     with pytest.raises(ModelError):
         parallel.run_batch_parallel(model, inputs, cfg, mode="optimized", prepared=bad)
+
+
+def _dist_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)  # one GPU on the test box: ranks share it over gloo
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        model, inputs = _edge(m=500)
+        data = np.asarray(inputs.data).copy()
+        data[:, 250:] *= 0.9  # skew: the second shard thins out faster
+        inputs = make_feature_batch(1024, data)
+        res, comm, bal = parallel.run_batch_parallel(
+            model, inputs, InferenceConfig(workers=world, rebalance_threshold=1.05))
+        q.put((rank, res.categories.tolist(),
+               [(o.active_before, o.active_after) for o in res.per_layer],
+               float(np.asarray(res.final.data, np.float64).sum()), comm.total_moved))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distributed_transport_two_ranks(cuda_ok):
+    """run_batch_parallel under torch.distributed (2 ranks on the test box's
+    single GPU, gloo wire): DistTransport + DeviceShard end to end."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    model, inputs = _edge(m=500)
+    data = np.asarray(inputs.data).copy()
+    data[:, 250:] *= 0.9
+    inputs = make_feature_batch(1024, data)
+    single = engine.infer(model, inputs, InferenceConfig())
+    for rank, cats, per_layer, vsum, moved in res:
+        assert cats == single.categories.tolist()
+        assert per_layer == [(o.active_before, o.active_after) for o in single.per_layer]
+        assert vsum == float(np.asarray(single.final.data, np.float64).sum())
+    assert res[0][1:] == res[1][1:]
