@@ -142,6 +142,22 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_traffic(cfg_key: str):
+    """DRAM bytes per launch of the layer kernel from the committed ncu capture
+    (profiles/*_ncu_layer*_<cfg>.json, one steady-state launch)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_ncu_layer*_{cfg_key}.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    try:
+        mb = float(d["dram__bytes_read.sum"][0]) + float(d["dram__bytes_write.sum"][0])
+    except (KeyError, TypeError, ValueError):
+        return None, None
+    return mb * 1e6, os.path.basename(files[-1])
+
+
 def cpu_baseline(model, inputs, sample_cols: int, threads: int):
     """The oracle port on the host cores, on the first `sample_cols` inputs."""
     from oracle import oracle
@@ -386,6 +402,7 @@ def run_ours(args, cfg):
     achieved = float(bytes_l[active].sum() / (layer_ms.mean(axis=0)[active].sum() / 1e3) / 1e9)
     peak, peak_src = measured_peaks()
     kernel_share = float(layer_ms.sum() / ms_total)
+    traffic, traffic_src = ncu_traffic(args.config)
 
     # ---- end to end through the public API: pinned host inputs -> categories
     pinned = torch.empty((m, n), dtype=torch.float32).pin_memory()
@@ -439,7 +456,10 @@ def run_ours(args, cfg):
                     "ms_per_step": e2e_s * 1e3,
                     "path": "engine.infer(values=False) on a pinned-host FeatureBatch"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": (f"profiles/{traffic_src}: dram read+write of one "
+                                            "steady-state launch (ncu --set full)")
+                                           if traffic else None,
                          "peak_source": peak_src,
                          "kernel": "layer_kernel (csrc/layer.cu)",
                          "bytes_per_launch": "8*N*M_l + 6*nnz_l + 4*N",
@@ -465,7 +485,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dump-layers", default="", help="write per-layer counts/times (JSON)")
     ap.add_argument("--plan", default="", help="layout knobs, e.g. max_groups=8,footprint_cap=96")
-    ap.add_argument("--cpu-sample", type=int, default=1024,
+    ap.add_argument("--cpu-sample", type=int, default=6144,
                     help="inputs in the CPU-baseline sample (0 = skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
