@@ -235,14 +235,19 @@ struct Rec<7> {
 };
 
 // acc[2k], acc[2k+1]: row k, features (4l, 4l+1) and (4l+2, 4l+3).
+// Records are walked with a bumped pointer; the feature row of a record is at
+// ybase + record.offset.
 template <int R, bool FMA, int UNROLL>
 __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int cnt,
                                            const char *ybase, u64 negz2) {
+  constexpr int RW = Rec<R>::W;
+  const uint32_t *rp = recs;
+  const uint32_t *const end = recs + cnt * RW;
 #pragma unroll UNROLL
-  for (int i = 0; i < cnt; i++) {
+  for (; rp < end; rp += RW) {
     uint32_t off;
     float w[R];
-    Rec<R>::load(recs + i * Rec<R>::W, off, w);
+    Rec<R>::load(rp, off, w);
     const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ybase + off);
 #pragma unroll
     for (int k = 0; k < R; k++) {
@@ -546,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       u64 acc[2 * R];
 #pragma unroll
       for (int r = 0; r < 2 * R; r++) acc[r] = 0ull;
-      accumulate<R, FMA, 2>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
+      accumulate<R, FMA, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
                             meta[seg_base + 2 * g + 1], ybase, negz2);
       if (h.nst > 1) accumulate_global<R, FMA>(A, acc, h.b, h.t, lane, M, negz2);
       epilogue<R, FMA>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
