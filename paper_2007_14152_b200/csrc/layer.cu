@@ -52,7 +52,8 @@ namespace {
 constexpr int kTile = SPDNN_TILE_FEATURES;  // 128
 constexpr int kRowBytes = SPDNN_STAGED_ROW_BYTES;
 constexpr int kConsumerWarps = 16;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kProducerWarps = 4;  // one per scheduler: the 4-byte gather path needs the issue slots
+constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
 constexpr int kMaxBufs = 4;  // ring depth: as many buffers as shared memory holds (<= 4)
 constexpr int kHeaderBytes = 128;  // keeps every region 128-byte aligned (TMA dst)
 
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ int s_done[kMaxBufs];
+  __shared__ int s_pitem;
 
   constexpr int RW = Rec<R>::W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -400,49 +402,50 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
-    // ======================= producer warp =======================
+  if (warp >= kConsumerWarps) {
+    // ======================= producer warps =======================
     // Per item (= ring fill): TMA bulk copies of the block's metadata and
     // union records and -- when the tile's 128 feature columns are contiguous
     // (the steady state: every tile after a layer without deaths) -- TMA
     // gather4 of the staged rows, 4 input neurons x 512 bytes per op. Tiles
     // with gaps left by features that died in the previous layer are
-    // gathered with 4-byte cp.async instead.
+    // gathered with 4-byte cp.async, the staged rows split over the
+    // producer warps (named barrier 1 keeps them in step).
+    const int pw = warp - kConsumerWarps;
+    const int ptid = pw * 32 + lane;
+    auto pbar = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(kProducerWarps * 32) : "memory"); };
     for (int k = 0;; k++) {
-      int item = 0;
-      if (lane == 0) item = atomicAdd(A.work, 1);
-      item = __shfl_sync(0xffffffffu, item, 0);
+      if (ptid == 0) s_pitem = atomicAdd(A.work, 1);
+      pbar();
+      const int item = s_pitem;
       if (item >= items) {
-        // no more work: end markers in the next nbuf entries. A consumer warp
-        // waits at most 16/gpi <= nbuf entries past the last one it served.
-        for (int e = 0; e < nbuf; e++, k++) {
-          const int slot = k % nbuf;
-          mbar_wait(empty0 + 8 * slot, ((uint32_t)(k / nbuf) & 1u) ^ 1u);
-          if (lane == 0) {
-            reinterpret_cast<Header *>(smem + slot * A.buf_bytes)->item = -1;
-            mbar_arrive(full0 + 8 * slot);
+        if (pw == 0) {
+          // end markers in the next nbuf entries. A consumer warp waits at
+          // most 16/gpi <= nbuf entries past the last one it served.
+          for (int e = 0; e < nbuf; e++, k++) {
+            const int slot = k % nbuf;
+            mbar_wait(empty0 + 8 * slot, ((uint32_t)(k / nbuf) & 1u) ^ 1u);
+            if (lane == 0) {
+              reinterpret_cast<Header *>(smem + slot * A.buf_bytes)->item = -1;
+              mbar_arrive(full0 + 8 * slot);
+            }
+            __syncwarp();
           }
-          __syncwarp();
         }
         break;
       }
-      const bool more = true;
-      int t = 0, b = 0, ng = 0, nst = 1;
-      int meta_off = 0, fp_cnt = 0, rec_off = 0, rec_cnt = 0;
-      if (more) {
-        t = item / nb;
-        b = item - t * nb;
-        const int v = lane < 8 ? __ldg(A.L.blocks + (int64_t)b * 8 + lane) : 0;
-        ng = __shfl_sync(0xffffffffu, v, 1);
-        nst = __shfl_sync(0xffffffffu, v, 2);
-        meta_off = __shfl_sync(0xffffffffu, v, 4);
-        fp_cnt = __shfl_sync(0xffffffffu, v, 5);
-        rec_off = __shfl_sync(0xffffffffu, v, 6);
-        rec_cnt = __shfl_sync(0xffffffffu, v, 7);
-      }
+      const int t = item / nb;
+      const int b = item - t * nb;
+      const int v = lane < 8 ? __ldg(A.L.blocks + (int64_t)b * 8 + lane) : 0;
+      const int ng = __shfl_sync(0xffffffffu, v, 1);
+      const int nst = __shfl_sync(0xffffffffu, v, 2);
+      const int meta_off = __shfl_sync(0xffffffffu, v, 4);
+      const int fp_cnt = __shfl_sync(0xffffffffu, v, 5);
+      const int rec_off = __shfl_sync(0xffffffffu, v, 6);
+      const int rec_cnt = __shfl_sync(0xffffffffu, v, 7);
       // feature columns 32q + lane (q < 4) of tile t: gathers then write 32
       // consecutive smem words per instruction (bank-conflict free)
-      const int valid = more ? min(kTile, M - t * kTile) : 0;
+      const int valid = min(kTile, M - t * kTile);
       int src[4];
       bool ok[4];
 #pragma unroll
@@ -465,50 +468,52 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       const uint32_t smeta = buf + kHeaderBytes;
       const uint32_t srec = smeta + A.meta_bytes;
       const uint32_t sy = srec + A.rec_bytes;
-      if (more) {
-        const int meta_words = ((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3);
-        const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
-        const int quads = (fp_cnt + 3) >> 2;
+      const int meta_words = ((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3);
+      const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
+      const int quads = (fp_cnt + 3) >> 2;
+      if (ptid == 0) {
         const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
                             (contig ? (uint32_t)quads * 4u * kRowBytes : 0u);
-        if (lane == 0) mbar_expect_tx(full, tx);
-        __syncwarp();
-        if (lane == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
-        if (lane == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
-        const int32_t *fp = A.L.meta + meta_off;
-        if (contig) {
-          for (int qd = lane; qd < quads; qd += 32) {
-            int4 c4;
-            if (4 * qd + 3 < fp_cnt) {
-              c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
-            } else {
-              c4.x = __ldg(fp + 4 * qd);
-              c4.y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : c4.x;
-              c4.z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : c4.x;
-              c4.w = c4.x;
-            }
-            tma_gather4(sy + (uint32_t)qd * 4u * kRowBytes, &A.tmap_in, p0, c4.x, c4.y, c4.z,
-                        c4.w, full);
-          }
-        } else {
-          for (int s0 = 0; s0 < fp_cnt; s0 += 32) {
-            const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
-            const int cnt = min(32, fp_cnt - s0);
-            for (int i = 0; i < cnt; i++) {
-              const int64_t c = __shfl_sync(0xffffffffu, my, i);
-              const float *row = A.y_in + c * A.ld;
-              const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 4 * lane;
-#pragma unroll
-              for (int q = 0; q < 4; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
-            }
-          }
-          mbar_cp_async_arrive_inc(full);
-        }
+        mbar_expect_tx(full, tx);
       }
-      __syncwarp();
-      if (lane == 0) {
+      pbar();  // expected bytes registered before any copy can complete
+      if (ptid == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
+      if (ptid == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
+      const int32_t *fp = A.L.meta + meta_off;
+      if (contig) {
+        for (int qd = ptid; qd < quads; qd += kProducerWarps * 32) {
+          int4 c4;
+          if (4 * qd + 3 < fp_cnt) {
+            c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
+          } else {
+            c4.x = __ldg(fp + 4 * qd);
+            c4.y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : c4.x;
+            c4.z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : c4.x;
+            c4.w = c4.x;
+          }
+          tma_gather4(sy + (uint32_t)qd * 4u * kRowBytes, &A.tmap_in, p0, c4.x, c4.y, c4.z, c4.w,
+                      full);
+        }
+      } else {
+        // staged rows s = pw, pw + P, ...: the warp's 32 lanes copy the row's
+        // 128 features (4 per lane)
+        for (int s0 = pw * 32; s0 < fp_cnt; s0 += kProducerWarps * 32) {
+          const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
+          const int cnt = min(32, fp_cnt - s0);
+          for (int i = 0; i < cnt; i++) {
+            const int64_t c = __shfl_sync(0xffffffffu, my, i);
+            const float *row = A.y_in + c * A.ld;
+            const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 4 * lane;
+#pragma unroll
+            for (int q = 0; q < 4; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
+          }
+        }
+        mbar_cp_async_arrive_inc(full);
+      }
+      pbar();  // every producer's copies issued and counted
+      if (ptid == 0) {
         Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
-        h->item = more ? item : -1;
+        h->item = item;
         h->t = t;
         h->b = b;
         h->stage = 0;
