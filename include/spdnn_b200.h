@@ -141,8 +141,8 @@ typedef struct spdnn_layer_dev {
 
 /* Per-inference scratch shared by every layer launch (device pointers). */
 typedef struct spdnn_scratch {
-  int32_t *tile_done;      /* [ceil(M_cap/128)] zero-initialised */
-  uint32_t *tile_alive;    /* [4*ceil(M_cap/128)] zero-initialised */
+  int32_t *tile_done;      /* [ceil(M_cap/64)] zero-initialised */
+  uint32_t *tile_alive;    /* [ceil(M_cap/32)] zero-initialised (one bit per feature) */
   int32_t *work;           /* [num_layers] zero-initialised work counters */
   uint32_t *guard;         /* [1] zero-initialised; bit 0 = FMA-form guard
                               tripped (rerun in the exact form), bit 1 =
@@ -158,6 +158,8 @@ typedef struct spdnn_scratch {
 typedef struct spdnn_run_opts {
   int32_t fma_form;
   float tiny;
+  int32_t features_per_lane; /* 4 (default, 128-feature items) or 2 (64-feature
+                                items, twice the resident consumer warps) */
 } spdnn_run_opts;
 
 /* One layer over the active features (engine.run_layer_step, engine.py:145-170):

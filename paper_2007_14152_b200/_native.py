@@ -56,7 +56,7 @@ class Scratch(ctypes.Structure):
 
 
 class RunOpts(ctypes.Structure):
-    _fields_ = [("fma_form", i32), ("tiny", ctypes.c_float)]
+    _fields_ = [("fma_form", i32), ("tiny", ctypes.c_float), ("features_per_lane", i32)]
 
 
 _lib = None

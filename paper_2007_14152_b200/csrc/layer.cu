@@ -49,11 +49,6 @@
 
 namespace {
 
-constexpr int kTile = SPDNN_TILE_FEATURES;  // 128
-constexpr int kRowBytes = SPDNN_STAGED_ROW_BYTES;
-constexpr int kConsumerWarps = 16;
-constexpr int kProducerWarps = 4;  // one per scheduler: the 4-byte gather path needs the issue slots
-constexpr int kThreads = (kConsumerWarps + kProducerWarps) * 32;
 constexpr int kMaxBufs = 4;  // ring depth: as many buffers as shared memory holds (<= 4)
 constexpr int kHeaderBytes = 128;  // keeps every region 128-byte aligned (TMA dst)
 
@@ -189,8 +184,9 @@ struct LayerArgs {
 // Ring-buffer header written by the producer (one per buffer fill).
 struct Header {
   int item;     // -1: no more work
+  int entry;    // ring entry number (stale-phase check)
   int t, b;
-  int stage, nst;
+  int nst;
   int ng;
   int rec_cnt;  // records of this stage (multi-stage: all belong to group 0)
   int fp_cnt;
@@ -238,10 +234,54 @@ struct Rec<7> {
 // acc[2k], acc[2k+1]: row k, features (4l, 4l+1) and (4l+2, 4l+3).
 // Records are walked with a bumped pointer; the feature row of a record is at
 // ybase + record.offset.
-template <int R, bool FMA, int UNROLL>
+// ---- per-configuration constants ---------------------------------------
+// FPL = fp32 features per lane (2 or 4): a work item covers 32 * FPL features;
+// a staged input neuron is a (128 * FPL)-byte smem row. FPL = 4 reuses every
+// weight over more features, FPL = 2 halves the accumulator registers and
+// buys twice the resident consumer warps.
+template <int FPL>
+struct Cfg;
+template <>
+struct Cfg<4> {
+  static constexpr int kConsumers = 16, kProducers = 4, kMaxRegs = 96;
+};
+template <>
+struct Cfg<2> {
+  static constexpr int kConsumers = 28, kProducers = 4, kMaxRegs = 64;
+};
+template <int FPL>
+struct Geo {
+  static constexpr int kTileF = 32 * FPL;      // features per item
+  static constexpr int kRow = 4 * kTileF;      // staged row bytes
+  static constexpr int kC = Cfg<FPL>::kConsumers;
+  static constexpr int kP = Cfg<FPL>::kProducers;
+  static constexpr int kThreads = (kC + kP) * 32;
+  // record offsets are slot * SPDNN_STAGED_ROW_BYTES (512): shift to this row size
+  static constexpr int kOffShift = FPL == 4 ? 0 : 1;
+};
+
+template <int FPL>
+struct YVec;
+template <>
+struct YVec<4> {
+  u64 v[2];
+  __device__ __forceinline__ void load(const char *p) {
+    const ulonglong2 t = *reinterpret_cast<const ulonglong2 *>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+  }
+};
+template <>
+struct YVec<2> {
+  u64 v[1];
+  __device__ __forceinline__ void load(const char *p) { v[0] = *reinterpret_cast<const u64 *>(p); }
+};
+
+// acc[(FPL/2)*k + h]: row k, features (FPL*l + 2h, FPL*l + 2h + 1).
+template <int R, bool FMA, int FPL, int UNROLL>
 __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int cnt,
                                            const char *ybase, u64 negz2) {
-  constexpr int RW = Rec<R>::W;
+  constexpr int RW = Rec<R>::W, H = FPL / 2;
   const uint32_t *rp = recs;
   const uint32_t *const end = recs + cnt * RW;
 #pragma unroll UNROLL
@@ -249,80 +289,75 @@ __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int c
     uint32_t off;
     float w[R];
     Rec<R>::load(rp, off, w);
-    const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ybase + off);
+    YVec<FPL> y;
+    y.load(ybase + (off >> Geo<FPL>::kOffShift));
 #pragma unroll
     for (int k = 0; k < R; k++) {
-      if (FMA) {
-        fma2_acc(acc[2 * k], y.x, w[k]);
-        fma2_acc(acc[2 * k + 1], y.y, w[k]);
-      } else {
-        mul_add2_acc(acc[2 * k], y.x, w[k], negz2);
-        mul_add2_acc(acc[2 * k + 1], y.y, w[k], negz2);
+#pragma unroll
+      for (int h = 0; h < H; h++) {
+        if (FMA) fma2_acc(acc[H * k + h], y.v[h], w[k]);
+        else mul_add2_acc(acc[H * k + h], y.v[h], w[k], negz2);
       }
     }
   }
 }
 
-// Bias, clamp, store, activity (+ FMA-form guard) for one finished group.
-// rows / bias were loaded before the accumulation (latency hidden).
-template <int R, bool FMA, bool FULL>
+// Bias, clamp, store for one finished group; returns the lane's activity bits.
+template <int R, bool FMA, int FPL, bool FULL>
 __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, const u64 *acc,
                                                 const int *rows, const float *bias, int j0,
                                                 int valid, bool &tiny) {
-  bool a0 = false, a1 = false, a2 = false, a3 = false;
+  constexpr int H = FPL / 2;
+  bool al[FPL];
+#pragma unroll
+  for (int q = 0; q < FPL; q++) al[q] = false;
 #pragma unroll
   for (int k = 0; k < R; k++) {
     if (rows[k] < 0) continue;
     const u64 b2 = pack2(bias[k], bias[k]);
-    float x0, x1, x2, x3;
-    unpack2(add2(acc[2 * k], b2), x0, x1);
-    unpack2(add2(acc[2 * k + 1], b2), x2, x3);
-    x0 = clamp32(x0);
-    x1 = clamp32(x1);
-    x2 = clamp32(x2);
-    x3 = clamp32(x3);
-    a0 |= x0 > 0.0f;
-    a1 |= x1 > 0.0f;
-    a2 |= x2 > 0.0f;
-    a3 |= x3 > 0.0f;
-    if (FMA) {
-      const uint32_t tb = A.tiny_bits_m1;
-      tiny |= (__float_as_uint(x0) - 1u < tb) && (FULL || 0 < valid);
-      tiny |= (__float_as_uint(x1) - 1u < tb) && (FULL || 1 < valid);
-      tiny |= (__float_as_uint(x2) - 1u < tb) && (FULL || 2 < valid);
-      tiny |= (__float_as_uint(x3) - 1u < tb) && (FULL || 3 < valid);
+    float x[FPL];
+#pragma unroll
+    for (int h = 0; h < H; h++) unpack2(add2(acc[H * k + h], b2), x[2 * h], x[2 * h + 1]);
+#pragma unroll
+    for (int q = 0; q < FPL; q++) {
+      x[q] = clamp32(x[q]);
+      al[q] |= x[q] > 0.0f;
+      if (FMA) tiny |= (__float_as_uint(x[q]) - 1u < A.tiny_bits_m1) && (FULL || q < valid);
     }
     float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
     if (FULL) {
-      *reinterpret_cast<float4 *>(dst) = make_float4(x0, x1, x2, x3);
+      if (FPL == 4) *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
+      else *reinterpret_cast<float2 *>(dst) = make_float2(x[0], x[1]);
     } else {
-      if (0 < valid) dst[0] = x0;
-      if (1 < valid) dst[1] = x1;
-      if (2 < valid) dst[2] = x2;
-      if (3 < valid) dst[3] = x3;
+#pragma unroll
+      for (int q = 0; q < FPL; q++)
+        if (q < valid) dst[q] = x[q];
     }
   }
-  uint32_t am = (a0 ? 1u : 0u) | (a1 ? 2u : 0u) | (a2 ? 4u : 0u) | (a3 ? 8u : 0u);
-  if (!FULL) am &= valid >= 4 ? 0xfu : (valid > 0 ? (1u << valid) - 1u : 0u);
+  uint32_t am = 0;
+#pragma unroll
+  for (int q = 0; q < FPL; q++) am |= al[q] ? (1u << q) : 0u;
+  if (!FULL) am &= valid >= FPL ? (1u << FPL) - 1u : (valid > 0 ? (1u << valid) - 1u : 0u);
   return am;
 }
 
-template <int R, bool FMA>
+template <int R, bool FMA, int FPL>
 __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, const int *rows,
                                          const float *bias, int t, int lane, int M,
                                          uint32_t *s_alive) {
-  const int j0 = t * kTile + 4 * lane;
+  constexpr int T = Geo<FPL>::kTileF, LPW = 32 / FPL;  // lanes per 32-feature mask word
+  const int j0 = t * T + FPL * lane;
   const int valid = M - j0;  // features of this lane that exist (may be <= 0)
   bool tiny = false;
-  const uint32_t am = (t + 1) * kTile <= M
-                          ? finish_rows<R, FMA, true>(A, acc, rows, bias, j0, valid, tiny)
-                          : finish_rows<R, FMA, false>(A, acc, rows, bias, j0, valid, tiny);
+  const uint32_t am = (t + 1) * T <= M
+                          ? finish_rows<R, FMA, FPL, true>(A, acc, rows, bias, j0, valid, tiny)
+                          : finish_rows<R, FMA, FPL, false>(A, acc, rows, bias, j0, valid, tiny);
   if (FMA && tiny) atomicOr(A.guard, 1u);
-  // word w of the 128-bit tile mask holds features 32w..32w+31 (lanes 8w..8w+7)
-  const uint32_t mine = am << (4 * (lane & 7));
+  // word w of the tile mask holds features 32w..32w+31 (lanes LPW*w .. LPW*w+LPW-1)
+  const uint32_t mine = am << (FPL * (lane % LPW));
 #pragma unroll
-  for (int w = 0; w < 4; w++) {
-    const uint32_t word = __reduce_or_sync(0xffffffffu, (lane >> 3) == w ? mine : 0u);
+  for (int w = 0; w < FPL; w++) {
+    const uint32_t word = __reduce_or_sync(0xffffffffu, lane / LPW == w ? mine : 0u);
     if (lane == 0 && word) atomicOr(&s_alive[w], word);
   }
 }
@@ -330,17 +365,17 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, con
 // Extra stages of a lone oversized group (rare: a row group whose inputs
 // exceed the staging caps): its records are consumed straight from global
 // memory, the feature values gathered through a_in. Slow, correct.
-template <int R, bool FMA>
+template <int R, bool FMA, int FPL>
 __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, int lane, int M,
                                   u64 negz2) {
-  constexpr int RW = Rec<R>::W;
+  constexpr int RW = Rec<R>::W, H = FPL / 2, T = Geo<FPL>::kTileF;
   const int nst = __ldg(A.L.blocks + (int64_t)b * 8 + 2);
   const int first_extra = __ldg(A.L.blocks + (int64_t)b * 8 + 3);
-  int pos[4];
-  bool ok[4];
+  int pos[FPL];
+  bool ok[FPL];
 #pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const int j = t * kTile + 4 * lane + q;
+  for (int q = 0; q < FPL; q++) {
+    const int j = t * T + FPL * lane + q;
     ok[q] = j < M;
     pos[q] = ok[q] ? __ldg(A.a_in + j) : 0;
   }
@@ -351,40 +386,40 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
       uint32_t off;
       float w[R];
       Rec<R>::load(recs + i * RW, off, w);  // (global loads)
-      const int64_t c = __ldg(A.L.meta + sd.x + off / kRowBytes);
+      const int64_t c = __ldg(A.L.meta + sd.x + off / SPDNN_STAGED_ROW_BYTES);
       const float *row = A.y_in + c * A.ld;
-      float v[4];
+      float v[FPL];
 #pragma unroll
-      for (int q = 0; q < 4; q++) v[q] = ok[q] ? __ldg(row + pos[q]) : 0.0f;
-      const u64 y01 = pack2(v[0], v[1]), y23 = pack2(v[2], v[3]);
+      for (int q = 0; q < FPL; q++) v[q] = ok[q] ? __ldg(row + pos[q]) : 0.0f;
 #pragma unroll
-      for (int k = 0; k < R; k++) {
-        if (FMA) {
-          fma2_acc(acc[2 * k], y01, w[k]);
-          fma2_acc(acc[2 * k + 1], y23, w[k]);
-        } else {
-          mul_add2_acc(acc[2 * k], y01, w[k], negz2);
-          mul_add2_acc(acc[2 * k + 1], y23, w[k], negz2);
+      for (int h = 0; h < H; h++) {
+        const u64 y = pack2(v[2 * h], v[2 * h + 1]);
+#pragma unroll
+        for (int k = 0; k < R; k++) {
+          if (FMA) fma2_acc(acc[H * k + h], y, w[k]);
+          else mul_add2_acc(acc[H * k + h], y, w[k], negz2);
         }
       }
     }
   }
 }
 
-template <int R, bool FMA>
-__global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constant__ LayerArgs A) {
+template <int R, bool FMA, int FPL>
+__global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
+    layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ int s_done[kMaxBufs];
   __shared__ int s_pitem;
 
-  constexpr int RW = Rec<R>::W;
+  using G = Geo<FPL>;
+  constexpr int RW = Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *A.m_in;
   if (M <= 0) return;
   const int nb = (int)A.L.num_blocks;
-  const int tiles = (M + kTile - 1) / kTile;
+  const int tiles = (M + T - 1) / T;
   const int items = tiles * nb;
   const int nbuf = A.nbuf, gpi = A.gpi;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
@@ -402,31 +437,33 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   }
   __syncthreads();
 
-  if (warp >= kConsumerWarps) {
+  if (warp >= C) {
     // ======================= producer warps =======================
     // Per item (= ring fill): TMA bulk copies of the block's metadata and
-    // union records and -- when the tile's 128 feature columns are contiguous
+    // union records and -- when the tile's feature columns are contiguous
     // (the steady state: every tile after a layer without deaths) -- TMA
-    // gather4 of the staged rows, 4 input neurons x 512 bytes per op. Tiles
+    // gather4 of the staged rows, 4 input neurons x T features per op. Tiles
     // with gaps left by features that died in the previous layer are
     // gathered with 4-byte cp.async, the staged rows split over the
     // producer warps (named barrier 1 keeps them in step).
-    const int pw = warp - kConsumerWarps;
+    const int pw = warp - C;
     const int ptid = pw * 32 + lane;
-    auto pbar = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(kProducerWarps * 32) : "memory"); };
+    auto pbar = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(P * 32) : "memory"); };
     for (int k = 0;; k++) {
       if (ptid == 0) s_pitem = atomicAdd(A.work, 1);
       pbar();
       const int item = s_pitem;
       if (item >= items) {
         if (pw == 0) {
-          // end markers in the next nbuf entries. A consumer warp waits at
-          // most 16/gpi <= nbuf entries past the last one it served.
+          // end markers in the next nbuf entries; a consumer warp waits at most
+          // ceil(C / gpi) <= nbuf entries past the last one it served
           for (int e = 0; e < nbuf; e++, k++) {
             const int slot = k % nbuf;
             mbar_wait(empty0 + 8 * slot, ((uint32_t)(k / nbuf) & 1u) ^ 1u);
             if (lane == 0) {
-              reinterpret_cast<Header *>(smem + slot * A.buf_bytes)->item = -1;
+              Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
+              h->item = -1;
+              h->entry = k;
               mbar_arrive(full0 + 8 * slot);
             }
             __syncwarp();
@@ -443,21 +480,21 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       const int fp_cnt = __shfl_sync(0xffffffffu, v, 5);
       const int rec_off = __shfl_sync(0xffffffffu, v, 6);
       const int rec_cnt = __shfl_sync(0xffffffffu, v, 7);
-      // feature columns 32q + lane (q < 4) of tile t: gathers then write 32
+      // feature columns 32q + lane (q < FPL) of tile t: gathers then write 32
       // consecutive smem words per instruction (bank-conflict free)
-      const int valid = min(kTile, M - t * kTile);
-      int src[4];
-      bool ok[4];
+      const int valid = min(T, M - t * T);
+      int src[FPL];
+      bool ok[FPL];
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
+      for (int q = 0; q < FPL; q++) {
         const int f = 32 * q + lane;
         ok[q] = f < valid;
-        src[q] = ok[q] ? __ldg(A.a_in + t * kTile + f) : 0;
+        src[q] = ok[q] ? __ldg(A.a_in + t * T + f) : 0;
       }
       const int p0 = __shfl_sync(0xffffffffu, src[0], 0);
       bool mine_contig = true;
 #pragma unroll
-      for (int q = 0; q < 4; q++) mine_contig &= !ok[q] || src[q] == p0 + 32 * q + lane;
+      for (int q = 0; q < FPL; q++) mine_contig &= !ok[q] || src[q] == p0 + 32 * q + lane;
       const bool contig = __all_sync(0xffffffffu, mine_contig) && (p0 & 3) == 0;
 
       const int slot = k % nbuf;
@@ -473,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       const int quads = (fp_cnt + 3) >> 2;
       if (ptid == 0) {
         const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
-                            (contig ? (uint32_t)quads * 4u * kRowBytes : 0u);
+                            (contig ? (uint32_t)quads * 4u * G::kRow : 0u);
         mbar_expect_tx(full, tx);
       }
       pbar();  // expected bytes registered before any copy can complete
@@ -481,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       if (ptid == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
       const int32_t *fp = A.L.meta + meta_off;
       if (contig) {
-        for (int qd = ptid; qd < quads; qd += kProducerWarps * 32) {
+        for (int qd = ptid; qd < quads; qd += P * 32) {
           int4 c4;
           if (4 * qd + 3 < fp_cnt) {
             c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
@@ -491,21 +528,20 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
             c4.z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : c4.x;
             c4.w = c4.x;
           }
-          tma_gather4(sy + (uint32_t)qd * 4u * kRowBytes, &A.tmap_in, p0, c4.x, c4.y, c4.z, c4.w,
+          tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c4.x, c4.y, c4.z, c4.w,
                       full);
         }
       } else {
-        // staged rows s = pw, pw + P, ...: the warp's 32 lanes copy the row's
-        // 128 features (4 per lane)
-        for (int s0 = pw * 32; s0 < fp_cnt; s0 += kProducerWarps * 32) {
+        // staged rows s = 32 pw .. : the warp's 32 lanes copy the row's T features
+        for (int s0 = pw * 32; s0 < fp_cnt; s0 += P * 32) {
           const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
           const int cnt = min(32, fp_cnt - s0);
           for (int i = 0; i < cnt; i++) {
             const int64_t c = __shfl_sync(0xffffffffu, my, i);
             const float *row = A.y_in + c * A.ld;
-            const uint32_t dst = sy + (uint32_t)(s0 + i) * kRowBytes + 4 * lane;
+            const uint32_t dst = sy + (uint32_t)(s0 + i) * G::kRow + 4 * lane;
 #pragma unroll
-            for (int q = 0; q < 4; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
+            for (int q = 0; q < FPL; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
           }
         }
         mbar_cp_async_arrive_inc(full);
@@ -514,9 +550,9 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       if (ptid == 0) {
         Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
         h->item = item;
+        h->entry = k;
         h->t = t;
         h->b = b;
-        h->stage = 0;
         h->nst = nst;
         h->ng = ng;
         h->rec_cnt = rec_cnt;
@@ -528,22 +564,29 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
   }
 
   // ======================= consumer warps =======================
-  // Work unit u = (item k = u / gpi, row group g = u % gpi); warp w takes
-  // units w, w + 16, ... so all warps stay busy whatever the group count per
-  // item, and items overlap in the ring.
+  // Work unit u = (ring entry k = u / gpi, row group g = u % gpi); warp w
+  // takes units w, w + C, ... Entries a warp waits on can be up to ceil(C/gpi)
+  // <= nbuf apart, so the slot's barrier may still be one phase behind: the
+  // header's entry number tells a stale phase from the awaited one.
   const u64 negz2 = pack2(A.negz, A.negz);
-  for (int u = warp;; u += kConsumerWarps) {
+  for (int u = warp;; u += C) {
     const int k = u / gpi, g = u - k * gpi;
     const int slot = k % nbuf;
     const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
-    mbar_wait(full0 + 8 * slot, phase);
     const char *buf = smem + slot * A.buf_bytes;
+    const volatile Header *vh = reinterpret_cast<const volatile Header *>(buf);
+    for (;;) {
+      mbar_wait(full0 + 8 * slot, phase);
+      if (vh->entry == k) break;
+      __nanosleep(256);  // the fill of entry k - nbuf is still in flight
+    }
+    mbar_wait(full0 + 8 * slot, phase);  // the phase of entry k itself
     const Header h = *reinterpret_cast<const Header *>(buf);
     if (h.item < 0) break;
     if (g < h.ng) {
       const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
       const uint32_t *recs = reinterpret_cast<const uint32_t *>(buf + kHeaderBytes + A.meta_bytes);
-      const char *ybase = buf + kHeaderBytes + A.meta_bytes + A.rec_bytes + 16 * lane;
+      const char *ybase = buf + kHeaderBytes + A.meta_bytes + A.rec_bytes + 4 * FPL * lane;
       const int seg_base = (h.fp_cnt + 3) & ~3;
       int rows[R];
       float bias[R];
@@ -553,13 +596,13 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
         rows[r] = mrows[r];
         bias[r] = rows[r] >= 0 ? __ldg(A.bias + rows[r]) : 0.0f;
       }
-      u64 acc[2 * R];
+      u64 acc[H * R];
 #pragma unroll
-      for (int r = 0; r < 2 * R; r++) acc[r] = 0ull;
-      accumulate<R, FMA, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
-                            meta[seg_base + 2 * g + 1], ybase, negz2);
-      if (h.nst > 1) accumulate_global<R, FMA>(A, acc, h.b, h.t, lane, M, negz2);
-      epilogue<R, FMA>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
+      for (int r = 0; r < H * R; r++) acc[r] = 0ull;
+      accumulate<R, FMA, FPL, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
+                                 meta[seg_base + 2 * g + 1], ybase, negz2);
+      if (h.nst > 1) accumulate_global<R, FMA, FPL>(A, acc, h.b, h.t, lane, M, negz2);
+      epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
     }
     __syncwarp();
     int bookkeeper = 0;
@@ -571,15 +614,15 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
     if (bookkeeper) {
       // every unit of the item has published its activity bits
       __threadfence_block();
-      uint32_t w4 = lane < 4 ? s_alive[slot][lane] : 0u;
+      uint32_t wv = lane < FPL ? s_alive[slot][lane] : 0u;
       __syncwarp();
-      if (lane < 4) s_alive[slot][lane] = 0u;
+      if (lane < FPL) s_alive[slot][lane] = 0u;
       if (lane == 0) s_done[slot] = 0;
       int last = 0;
-      if (lane < 4 && w4) atomicOr(&A.tile_alive[4 * h.t + lane], w4);
+      if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * h.t + lane], wv);
       __syncwarp();
       if (lane == 0) {
-        // release: our tile_alive bits before the count; the last arrival
+        // release our activity bits before the count; the last arrival
         // acquires everyone's (acq_rel instead of a full __threadfence)
         int old;
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n"
@@ -590,27 +633,32 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        if (lane < 4) {
-          w4 = atomicOr(&A.tile_alive[4 * h.t + lane], 0u);
-          A.tile_alive[4 * h.t + lane] = 0u;
+        if (lane < FPL) {
+          wv = atomicOr(&A.tile_alive[FPL * h.t + lane], 0u);
+          A.tile_alive[FPL * h.t + lane] = 0u;
         }
         if (lane == 0) A.tile_done[h.t] = 0;
-        const uint32_t m0 = __shfl_sync(0xffffffffu, w4, 0), m1 = __shfl_sync(0xffffffffu, w4, 1);
-        const uint32_t m2 = __shfl_sync(0xffffffffu, w4, 2), m3 = __shfl_sync(0xffffffffu, w4, 3);
-        const int c0 = __popc(m0), c1 = __popc(m1), c2 = __popc(m2), c3 = __popc(m3);
-        int base = 0;
-        if (lane == 0 && c0 + c1 + c2 + c3) base = atomicAdd(A.m_out, c0 + c1 + c2 + c3);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const uint32_t mw[4] = {m0, m1, m2, m3};
-        const int pre[4] = {0, c0, c0 + c1, c0 + c1 + c2};
+        uint32_t mw[FPL];
+        int cnt[FPL], tot = 0;
 #pragma unroll
-        for (int w = 0; w < 4; w++) {
+        for (int w = 0; w < FPL; w++) {
+          mw[w] = __shfl_sync(0xffffffffu, wv, w);
+          cnt[w] = __popc(mw[w]);
+          tot += cnt[w];
+        }
+        int base = 0;
+        if (lane == 0 && tot) base = atomicAdd(A.m_out, tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        int pre = 0;
+#pragma unroll
+        for (int w = 0; w < FPL; w++) {
           if ((mw[w] >> lane) & 1u) {
-            const int rank = pre[w] + __popc(mw[w] & ((1u << lane) - 1u));
-            const int j = h.t * kTile + 32 * w + lane;
+            const int rank = pre + __popc(mw[w] & ((1u << lane) - 1u));
+            const int j = h.t * T + 32 * w + lane;
             A.a_out[base + rank] = j;
             A.cat_out[base + rank] = A.cat_in[j];
           }
+          pre += cnt[w];
         }
       }
     }
@@ -620,10 +668,16 @@ __global__ void __launch_bounds__(kThreads, 1) layer_kernel(const __grid_constan
 
 // ---- launch configuration ---------------------------------------------------
 
-template <int R>
+template <int R, int FPL>
 void *kernel_ptr(bool fma) {
-  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true>)
-             : reinterpret_cast<void *>(&layer_kernel<R, false>);
+  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true, FPL>)
+             : reinterpret_cast<void *>(&layer_kernel<R, false, FPL>);
+}
+
+template <int FPL>
+void *kernel_for(int R, bool fma) {
+  return R == 1 ? kernel_ptr<1, FPL>(fma)
+                : (R == 3 ? kernel_ptr<3, FPL>(fma) : (R == 7 ? kernel_ptr<7, FPL>(fma) : nullptr));
 }
 
 struct DevInfo {
@@ -650,11 +704,11 @@ int device_info(int &sms, size_t &optin) {
   return 0;
 }
 
+template <int FPL>
 int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
+  using G = Geo<FPL>;
   const spdnn_layer_dev &L = A.L;
-  const int R = L.rows_per_group;
-  void *fn = R == 1 ? kernel_ptr<1>(fma)
-                    : (R == 3 ? kernel_ptr<3>(fma) : (R == 7 ? kernel_ptr<7>(fma) : nullptr));
+  void *fn = kernel_for<FPL>(L.rows_per_group, fma);
   if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1, 3 or 7");
   int sms;
   size_t optin;
@@ -662,20 +716,14 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   auto up128 = [](size_t x) { return (x + 127) / 128 * 128; };
   const size_t meta = up128((size_t)L.max_meta_per_block * 4);
   const size_t rec = up128((size_t)L.max_records_per_stage * L.record_words * 4 + 16);
-  const size_t ys = (size_t)((L.max_fp_per_stage + 3) & ~3) * kRowBytes;  // gather4: rows in 4s
+  const size_t ys = (size_t)((L.max_fp_per_stage + 3) & ~3) * G::kRow;  // gather4: rows in 4s
   const size_t buf = (kHeaderBytes + meta + rec + ys + 127) / 128 * 128;
   const size_t budget = optin - 2048;  // static shared memory + reserve
-  // Ring depth and units per item. Consumer warp w visits every (16/gpi)-th
-  // ring entry; with nbuf a multiple of 16/gpi it has itself consumed entry
-  // k - nbuf before it waits on entry k, so an mbarrier phase can never be
-  // mistaken for the one nbuf entries earlier.
-  int nbuf = (int)std::min<size_t>(kMaxBufs, budget / buf);
-  if (nbuf == 3) nbuf = 2;
+  const int nbuf = (int)std::min<size_t>(kMaxBufs, budget / buf);
   if (nbuf < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
-  int gpi = 1;
-  while (gpi < L.max_groups_per_block) gpi *= 2;
-  gpi = std::max(gpi, kConsumerWarps / nbuf);
-  if (gpi > kConsumerWarps) return spdnn_fail(SPDNN_EINVAL, "layer: more row groups per block than warps");
+  // units per item: at least the block's groups, and enough that a consumer
+  // warp's consecutive units are at most nbuf ring entries apart
+  const int gpi = std::max(std::max(1, L.max_groups_per_block), (G::kC + nbuf - 1) / nbuf);
   const size_t smem = (size_t)nbuf * buf;
   A.meta_bytes = (uint32_t)meta;
   A.rec_bytes = (uint32_t)rec;
@@ -685,11 +733,11 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, G::kThreads, smem);
   if (e != cudaSuccess || per_sm < 1)
     return spdnn_fail(SPDNN_ECUDA, "layer: kernel does not fit on an SM");
   void *args[] = {&A};
-  e = cudaLaunchKernel(fn, dim3(sms * per_sm), dim3(kThreads), args, smem, stream);
+  e = cudaLaunchKernel(fn, dim3(sms * per_sm), dim3(G::kThreads), args, smem, stream);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   return SPDNN_OK;
 }
@@ -766,12 +814,12 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 
 // y [n][ld] fp32 as a 2-D tensor whose box is one 128-feature row segment:
 // the producer's gather4 fetches 4 such rows (4 input neurons) per TMA op.
-int make_tensor_map(const float *y, int64_t n, int64_t ld, CUtensorMap *out) {
+int make_tensor_map(const float *y, int64_t n, int64_t ld, int box_cols, CUtensorMap *out) {
   auto enc = tensor_map_encoder();
   if (!enc) return spdnn_fail(SPDNN_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)n};
   cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(float)};
-  cuuint32_t box[2] = {(cuuint32_t)kTile, 1u};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, 1u};
   cuuint32_t estr[2] = {1u, 1u};
   CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(y), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -782,20 +830,20 @@ int make_tensor_map(const float *y, int64_t n, int64_t ld, CUtensorMap *out) {
 
 struct TmapCache {
   std::mutex mu;
-  std::map<std::tuple<const float *, int64_t, int64_t>, CUtensorMap> maps;
+  std::map<std::tuple<const float *, int64_t, int64_t, int>, CUtensorMap> maps;
 };
 TmapCache g_tmaps;
 
-int tensor_map_for(const float *y, int64_t n, int64_t ld, CUtensorMap *out) {
+int tensor_map_for(const float *y, int64_t n, int64_t ld, int box_cols, CUtensorMap *out) {
   std::lock_guard<std::mutex> lk(g_tmaps.mu);
-  auto key = std::make_tuple(y, n, ld);
+  auto key = std::make_tuple(y, n, ld, box_cols);
   auto it = g_tmaps.maps.find(key);
   if (it != g_tmaps.maps.end()) {
     *out = it->second;
     return SPDNN_OK;
   }
   if (g_tmaps.maps.size() > 64) g_tmaps.maps.clear();
-  int rc = make_tensor_map(y, n, ld, out);
+  int rc = make_tensor_map(y, n, ld, box_cols, out);
   if (rc == SPDNN_OK) g_tmaps.maps[key] = *out;
   return rc;
 }
@@ -805,7 +853,7 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
             int32_t *a_out, int64_t *cat_out, int32_t *m_out, const spdnn_scratch *scratch,
             int32_t *work, const spdnn_run_opts *opts, void *stream) {
   if (!layer || !bias || !y_in || !y_out || !a_in || !cat_in || !m_in || !a_out ||
-      !cat_out || !m_out || !scratch || !work || ld < 1 || ld % kTile)
+      !cat_out || !m_out || !scratch || !work || ld < 1 || ld % SPDNN_TILE_FEATURES)
     return spdnn_fail(SPDNN_EINVAL, "spdnn_layer_forward: bad argument");
   const bool fma = opts && opts->fma_form;
   if (fma && !scratch->guard)
@@ -813,7 +861,8 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   if (layer->num_blocks == 0) return SPDNN_OK;  // N == 0
   LayerArgs A;
   std::memset(&A, 0, sizeof(A));
-  int rc = tensor_map_for(y_in, layer->neurons, ld, &A.tmap_in);
+  const int fpl = (opts && opts->features_per_lane == 2) ? 2 : 4;
+  int rc = tensor_map_for(y_in, layer->neurons, ld, 32 * fpl, &A.tmap_in);
   if (rc) return rc;
   A.L = *layer;
   A.bias = bias;
@@ -835,7 +884,8 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   std::memcpy(&tb, &A.tiny, 4);
   A.tiny_bits_m1 = tb ? tb - 1u : 0u;
   A.negz = -0.0f;
-  return launch_layer(A, fma, (cudaStream_t)stream);
+  return fpl == 2 ? launch_layer<2>(A, fma, (cudaStream_t)stream)
+                  : launch_layer<4>(A, fma, (cudaStream_t)stream);
 }
 
 }  // namespace
@@ -893,7 +943,7 @@ extern "C" int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int
 extern "C" int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_sm,
                                      int32_t *threads_per_cta) {
   (void)rows_per_group;
-  if (threads_per_cta) *threads_per_cta = kThreads;
+  if (threads_per_cta) *threads_per_cta = Geo<4>::kThreads;
   if (ctas_per_sm) *ctas_per_sm = 1;
   return SPDNN_OK;
 }

@@ -315,9 +315,8 @@ class Workspace:
         self.a = [torch.empty(self.ld, dtype=i32, device=device) for _ in range(2)]
         self.cat = [torch.empty(self.ld, dtype=i64, device=device) for _ in range(2)]
         self.counts = torch.zeros(num_layers + 1, dtype=i32, device=device)
-        tiles = self.ld // TILE
-        self.tile_done = torch.zeros(tiles, dtype=i32, device=device)
-        self.tile_alive = torch.zeros(4 * tiles, dtype=i32, device=device)
+        self.tile_done = torch.zeros(self.ld // 64, dtype=i32, device=device)
+        self.tile_alive = torch.zeros(self.ld // 32, dtype=i32, device=device)
         self.work = torch.zeros(max(1, num_layers), dtype=i32, device=device)
         self.guard = torch.zeros(1, dtype=i32, device=device)
         self.scratch = _native.Scratch(self.tile_done.data_ptr(), self.tile_alive.data_ptr(),
@@ -408,9 +407,12 @@ def stage_inputs(ws: Workspace, x_host_or_dev, categories, net: "DeviceNetwork |
         ws.cat[0][:m].copy_(categories, non_blocking=True)
 
 
+FEATURES_PER_LANE = int(__import__("os").environ.get("SPDNN_FEATURES_PER_LANE", "4"))
+
+
 def run_opts(net: DeviceNetwork, fma: bool | None = None) -> _native.RunOpts:
     use = net.pow2 if fma is None else (fma and net.pow2)
-    return _native.RunOpts(int(use), net.tiny)
+    return _native.RunOpts(int(use), net.tiny, FEATURES_PER_LANE)
 
 
 def run_layers(net: DeviceNetwork, ws: Workspace, m0: int, fma: bool | None = None
