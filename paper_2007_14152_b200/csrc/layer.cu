@@ -145,6 +145,17 @@ __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap *tm
       "r"(bar)
       : "memory");
 }
+// L2 prefetch of the same 4 x box rows (no smem, no completion)
+__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap *tmap, int col, int r0,
+                                                     int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n"
+      ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void *gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gsrc), "r"(bytes) : "memory");
+}
 // TMA bulk copy global -> this CTA's shared memory, completion as tx bytes
 __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32_t bytes,
                                          uint32_t bar) {
@@ -178,6 +189,7 @@ struct LayerArgs {
   uint32_t meta_bytes;
   uint32_t rec_bytes;
   int nbuf;            // ring depth
+  int simple_wait;     // 1: consumer warps visit every (C/gpi)-th entry and (C/gpi) | nbuf
   int gpi;             // consumer work units (row groups) per item = max groups per block
 };
 
@@ -449,10 +461,40 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
     const int pw = warp - C;
     const int ptid = pw * 32 + lane;
     auto pbar = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(P * 32) : "memory"); };
+    if (ptid == 0) s_pitem = atomicAdd(A.work, 1);
+    pbar();
+    int next_item = s_pitem;
     for (int k = 0;; k++) {
+      const int item = next_item;
+      pbar();  // everyone has read s_pitem
       if (ptid == 0) s_pitem = atomicAdd(A.work, 1);
       pbar();
-      const int item = s_pitem;
+      next_item = s_pitem;
+      // L2 prefetch of the following item's rows, records and metadata so
+      // its smem fill (after a slot frees up) streams from L2
+      if (next_item < items) {
+        const int t2 = next_item / nb, b2 = next_item - t2 * nb;
+        const int4 d2 = __ldg(reinterpret_cast<const int4 *>(A.L.blocks + (int64_t)b2 * 8 + 4));
+        const int p2 = __ldg(A.a_in + t2 * T);
+        const int fc2 = d2.y, quads2 = (fc2 + 3) >> 2;
+        if (ptid == 0 && d2.w) bulk_prefetch_l2(A.L.records + (int64_t)d2.z * RW,
+                                                (uint32_t)((d2.w * RW * 4 + 15) & ~15));
+        if ((p2 & 3) == 0) {
+          const int32_t *fp2 = A.L.meta + d2.x;
+          for (int qd = ptid; qd < quads2; qd += P * 32) {
+            int4 c4;
+            if (4 * qd + 3 < fc2) {
+              c4 = __ldg(reinterpret_cast<const int4 *>(fp2) + qd);
+            } else {
+              c4.x = __ldg(fp2 + 4 * qd);
+              c4.y = 4 * qd + 1 < fc2 ? __ldg(fp2 + 4 * qd + 1) : c4.x;
+              c4.z = 4 * qd + 2 < fc2 ? __ldg(fp2 + 4 * qd + 2) : c4.x;
+              c4.w = c4.x;
+            }
+            tma_prefetch_gather4(&A.tmap_in, p2, c4.x, c4.y, c4.z, c4.w);
+          }
+        }
+      }
       if (item >= items) {
         if (pw == 0) {
           // end markers in the next nbuf entries; a consumer warp waits at most
@@ -575,12 +617,16 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
     const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
     const char *buf = smem + slot * A.buf_bytes;
     const volatile Header *vh = reinterpret_cast<const volatile Header *>(buf);
-    for (;;) {
+    if (A.simple_wait) {
       mbar_wait(full0 + 8 * slot, phase);
-      if (vh->entry == k) break;
-      __nanosleep(256);  // the fill of entry k - nbuf is still in flight
+    } else {
+      for (;;) {
+        mbar_wait(full0 + 8 * slot, phase);
+        if (vh->entry == k) break;
+        __nanosleep(256);  // the fill of entry k - nbuf is still in flight
+      }
+      mbar_wait(full0 + 8 * slot, phase);  // the phase of entry k itself
     }
-    mbar_wait(full0 + 8 * slot, phase);  // the phase of entry k itself
     const Header h = *reinterpret_cast<const Header *>(buf);
     if (h.item < 0) break;
     if (g < h.ng) {
@@ -730,6 +776,9 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   A.buf_bytes = (uint32_t)buf;
   A.nbuf = nbuf;
   A.gpi = gpi;
+  // warp w visits entries w/gpi + j*(C/gpi): when that stride divides nbuf the
+  // warp consumed entry k - nbuf itself before waiting on k (no stale phase)
+  A.simple_wait = (G::kC % gpi == 0 && nbuf % (G::kC / gpi) == 0) ? 1 : 0;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   int per_sm = 0;
