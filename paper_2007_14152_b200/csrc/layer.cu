@@ -145,17 +145,6 @@ __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap *tm
       "r"(bar)
       : "memory");
 }
-// L2 prefetch of the same 4 x box rows (no smem, no completion)
-__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap *tmap, int col, int r0,
-                                                     int r1, int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n"
-      ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_prefetch_l2(const void *gsrc, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gsrc), "r"(bytes) : "memory");
-}
 // TMA bulk copy global -> this CTA's shared memory, completion as tx bytes
 __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32_t bytes,
                                          uint32_t bar) {
@@ -461,40 +450,10 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
     const int pw = warp - C;
     const int ptid = pw * 32 + lane;
     auto pbar = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(P * 32) : "memory"); };
-    if (ptid == 0) s_pitem = atomicAdd(A.work, 1);
-    pbar();
-    int next_item = s_pitem;
     for (int k = 0;; k++) {
-      const int item = next_item;
-      pbar();  // everyone has read s_pitem
       if (ptid == 0) s_pitem = atomicAdd(A.work, 1);
       pbar();
-      next_item = s_pitem;
-      // L2 prefetch of the following item's rows, records and metadata so
-      // its smem fill (after a slot frees up) streams from L2
-      if (next_item < items) {
-        const int t2 = next_item / nb, b2 = next_item - t2 * nb;
-        const int4 d2 = __ldg(reinterpret_cast<const int4 *>(A.L.blocks + (int64_t)b2 * 8 + 4));
-        const int p2 = __ldg(A.a_in + t2 * T);
-        const int fc2 = d2.y, quads2 = (fc2 + 3) >> 2;
-        if (ptid == 0 && d2.w) bulk_prefetch_l2(A.L.records + (int64_t)d2.z * RW,
-                                                (uint32_t)((d2.w * RW * 4 + 15) & ~15));
-        if ((p2 & 3) == 0) {
-          const int32_t *fp2 = A.L.meta + d2.x;
-          for (int qd = ptid; qd < quads2; qd += P * 32) {
-            int4 c4;
-            if (4 * qd + 3 < fc2) {
-              c4 = __ldg(reinterpret_cast<const int4 *>(fp2) + qd);
-            } else {
-              c4.x = __ldg(fp2 + 4 * qd);
-              c4.y = 4 * qd + 1 < fc2 ? __ldg(fp2 + 4 * qd + 1) : c4.x;
-              c4.z = 4 * qd + 2 < fc2 ? __ldg(fp2 + 4 * qd + 2) : c4.x;
-              c4.w = c4.x;
-            }
-            tma_prefetch_gather4(&A.tmap_in, p2, c4.x, c4.y, c4.z, c4.w);
-          }
-        }
-      }
+      const int item = s_pitem;
       if (item >= items) {
         if (pw == 0) {
           // end markers in the next nbuf entries; a consumer warp waits at most
