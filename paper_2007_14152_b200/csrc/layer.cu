@@ -62,15 +62,24 @@ __device__ __forceinline__ u64 pack2(float a, float b) {
 __device__ __forceinline__ void unpack2(u64 v, float &a, float &b) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
 }
-// acc = y * w + acc in place (the "+l" tie keeps the accumulator register)
+// acc = y * w + acc in place. The CUDA intrinsic (not inline asm) lets the
+// register allocator keep each accumulator in place (inline-asm "+l" operands
+// cost 7 IMAD.MOV per record on the FMA pipe).
 __device__ __forceinline__ void fma2_acc(u64 &acc, u64 y, float w) {
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(y), "l"(pack2(w, w)));
+  float2 a = *reinterpret_cast<float2 *>(&acc);
+  const float2 yy = *reinterpret_cast<const float2 *>(&y);
+  a = __ffma2_rn(yy, make_float2(w, w), a);
+  acc = *reinterpret_cast<u64 *>(&a);
 }
-// acc = acc + fl(y * w): product rounded first (fma with a -0 addend), exact form
+// acc = acc + fl(y * w): the product rounded first. ptxas contracts even
+// __fmul2_rn + __fadd2_rn into one FFMA2 (CUDA 12.9), so the product is an
+// fma with a -0 addend the compiler cannot see (x + -0 == x for every x).
 __device__ __forceinline__ void mul_add2_acc(u64 &acc, u64 y, float w, u64 negz2) {
-  u64 p;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(y), "l"(pack2(w, w)), "l"(negz2));
-  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(p));
+  float2 a = *reinterpret_cast<float2 *>(&acc);
+  const float2 yy = *reinterpret_cast<const float2 *>(&y);
+  const float2 p = __ffma2_rn(yy, make_float2(w, w), *reinterpret_cast<const float2 *>(&negz2));
+  a = __fadd2_rn(a, p);
+  acc = *reinterpret_cast<u64 *>(&a);
 }
 __device__ __forceinline__ u64 add2(u64 a, u64 b) {
   u64 r;
