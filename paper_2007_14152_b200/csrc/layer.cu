@@ -312,27 +312,53 @@ __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int c
   }
 }
 
+// NaN-propagating max / min (max.NaN.f32): the reference's comparison clamp
+// `v < 0 -> 0, v > 32 -> 32` keeps NaN; v is never -0 (the accumulator starts
+// at +0 and round-to-nearest sums never produce -0), so max(v, +0) == v there.
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float min_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
 // Bias, clamp, store for one finished group; returns the lane's activity bits.
+// All rows are finished into the accumulator registers first and stored
+// after, so no store's source registers are overwritten while it is queued.
 template <int R, bool FMA, int FPL, bool FULL>
-__device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, const u64 *acc,
-                                                const int *rows, const float *bias, int j0,
-                                                int valid, bool &tiny) {
+__device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, const int *rows,
+                                                const float *bias, int j0, int valid,
+                                                bool &tiny) {
   constexpr int H = FPL / 2;
-  bool al[FPL];
+  float mx[FPL];
+  uint32_t mn = 0xffffffffu;  // min over outputs of bits(v) - 1: v in (0, tiny) check
 #pragma unroll
-  for (int q = 0; q < FPL; q++) al[q] = false;
+  for (int q = 0; q < FPL; q++) mx[q] = 0.0f;
+#pragma unroll
+  for (int k = 0; k < R; k++) {
+    const float2 b2 = make_float2(bias[k], bias[k]);
+#pragma unroll
+    for (int h = 0; h < H; h++) {
+      float2 v = __fadd2_rn(*reinterpret_cast<float2 *>(&acc[H * k + h]), b2);
+      v.x = min_nan(max_nan(v.x, 0.0f), 32.0f);
+      v.y = min_nan(max_nan(v.y, 0.0f), 32.0f);
+      *reinterpret_cast<float2 *>(&acc[H * k + h]) = v;
+    }
+  }
 #pragma unroll
   for (int k = 0; k < R; k++) {
     if (rows[k] < 0) continue;
-    const u64 b2 = pack2(bias[k], bias[k]);
-    float x[FPL];
-#pragma unroll
-    for (int h = 0; h < H; h++) unpack2(add2(acc[H * k + h], b2), x[2 * h], x[2 * h + 1]);
+    const float *x = reinterpret_cast<const float *>(&acc[H * k]);
 #pragma unroll
     for (int q = 0; q < FPL; q++) {
-      x[q] = clamp32(x[q]);
-      al[q] |= x[q] > 0.0f;
-      if (FMA) tiny |= (__float_as_uint(x[q]) - 1u < A.tiny_bits_m1) && (FULL || q < valid);
+      if (FULL || q < valid) {
+        mx[q] = fmaxf(mx[q], x[q]);
+        if (FMA) mn = min(mn, __float_as_uint(x[q]) - 1u);
+      }
     }
     float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
     if (FULL) {
@@ -344,15 +370,15 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, const u64 *a
         if (q < valid) dst[q] = x[q];
     }
   }
+  if (FMA) tiny = mn < A.tiny_bits_m1;
   uint32_t am = 0;
 #pragma unroll
-  for (int q = 0; q < FPL; q++) am |= al[q] ? (1u << q) : 0u;
-  if (!FULL) am &= valid >= FPL ? (1u << FPL) - 1u : (valid > 0 ? (1u << valid) - 1u : 0u);
+  for (int q = 0; q < FPL; q++) am |= mx[q] > 0.0f ? (1u << q) : 0u;
   return am;
 }
 
 template <int R, bool FMA, int FPL>
-__device__ __forceinline__ void epilogue(const LayerArgs &A, const u64 *acc, const int *rows,
+__device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int *rows,
                                          const float *bias, int t, int lane, int M,
                                          uint32_t *s_alive) {
   constexpr int T = Geo<FPL>::kTileF, LPW = 32 / FPL;  // lanes per 32-feature mask word
@@ -509,7 +535,7 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
 
       const int slot = k % nbuf;
       const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
-      mbar_wait(empty0 + 8 * slot, phase ^ 1u);
+      if (pw == 0) mbar_wait(empty0 + 8 * slot, phase ^ 1u);  // others park at the bar.sync below
       const uint32_t full = full0 + 8 * slot;
       const uint32_t buf = sbase + slot * A.buf_bytes;
       const uint32_t smeta = buf + kHeaderBytes;
