@@ -158,16 +158,26 @@ def ncu_traffic(cfg_key: str):
     return mb * 1e6, os.path.basename(files[-1])
 
 
-def cpu_baseline(model, inputs, sample_cols: int, threads: int):
-    """The oracle port on the host cores, on the first `sample_cols` inputs."""
+def cpu_baseline(model, inputs, sample_cols: int, threads: int, target_s: float = 0.0):
+    """The oracle port on the host cores, on the first `sample_cols` inputs.
+    With target_s > 0 the sample is first calibrated on a small slice and
+    grown to about target_s seconds of CPU work (bounded by the batch)."""
     from oracle import oracle
     from paper_2007_14152_b200.model import make_feature_batch
+    m_all = inputs.active_count
+    if target_s > 0:
+        probe = min(m_all, max(threads * 4, 64))
+        sub = make_feature_batch(model.neurons, np.asfortranarray(inputs.data[:, :probe]))
+        t0 = time.perf_counter()
+        oracle.infer(model, sub, threads=threads, want_final=False)
+        per_col = (time.perf_counter() - t0) / probe
+        sample_cols = int(min(m_all, max(probe, target_s / max(per_col, 1e-9))))
     sub = make_feature_batch(model.neurons, np.asfortranarray(inputs.data[:, :sample_cols]))
     t0 = time.perf_counter()
     r = oracle.infer(model, sub, threads=threads, want_final=False)
     dt = time.perf_counter() - t0
     edges = sample_cols * sum(l.nnz for l in model.layers)
-    return dict(value=edges / dt / 1e12, seconds=dt, counts=r.counts)
+    return dict(value=edges / dt / 1e12, seconds=dt, counts=r.counts, sample_cols=sample_cols)
 
 
 def run_reference(args, cfg):
@@ -177,11 +187,10 @@ def run_reference(args, cfg):
     model, inputs = build_workload(cfg)
     threads = os.cpu_count() or 1
     sample = args.cpu_sample
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        cpu_baseline(model, inputs, max(threads, sample // 16), threads)
     vals, secs = [], []
     for _ in range(args.steps):
-        r = cpu_baseline(model, inputs, sample, threads)
+        r = cpu_baseline(model, inputs, sample, threads, target_s=args.cpu_seconds)
+        sample = r["sample_cols"]
         vals.append(r["value"])
         secs.append(r["seconds"])
     v = float(np.median(vals))
@@ -431,10 +440,10 @@ def run_ours(args, cfg):
         cpu = None
         if world == 1 and args.cpu_sample > 0:
             threads = os.cpu_count() or 1
-            r = cpu_baseline(model, inputs, args.cpu_sample, threads)
-            # the sampled inputs must reproduce the GPU's per-input fate
+            r = cpu_baseline(model, inputs, args.cpu_sample, threads,
+                             target_s=args.cpu_seconds)
             cpu = {"value": r["value"], "unit": "TE/s", "cores": threads, "kind": "port",
-                   "sample": f"first {args.cpu_sample} of {cfg['inputs']} inputs, all "
+                   "sample": f"first {r['sample_cols']} of {cfg['inputs']} inputs, all "
                              f"{L} layers, oracle/spdnn_oracle.c on {threads} host threads "
                              f"({r['seconds']:.1f} s)"}
         line = {
@@ -485,8 +494,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dump-layers", default="", help="write per-layer counts/times (JSON)")
     ap.add_argument("--plan", default="", help="layout knobs, e.g. max_groups=8,footprint_cap=96")
-    ap.add_argument("--cpu-sample", type=int, default=6144,
-                    help="inputs in the CPU-baseline sample (0 = skip)")
+    ap.add_argument("--cpu-sample", type=int, default=1024,
+                    help="inputs in the CPU-baseline sample (0 = skip the CPU leg)")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="grow the CPU sample to about this much CPU time (0 = fixed sample)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")

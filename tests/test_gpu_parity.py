@@ -260,3 +260,24 @@ def test_nonfinite_inputs_rerun_unpadded(cuda_ok):
     assert np.array_equal(np.isnan(a), np.isnan(b))
     ok = ~np.isnan(a)
     assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))
+
+
+@pytest.mark.slow
+def test_config3_full_network_sampled_columns(cuda_ok):
+    """BASELINE.json configs[2] network at full size (16384 neurons x 1920
+    layers, bias -0.4, density 0.4): the GPU run of 4096 inputs agrees with the
+    oracle on a fixed-seed sample of 96 of them (columns are independent, so
+    the sample's categories and values must match exactly)."""
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=16384, layers=1920, connections_per_neuron=32, bias_value=-0.4, seed=1))
+    inputs = ingest.generate_synthetic_inputs(16384, 4096, 0.4, seed=2)
+    res = engine.infer(model, inputs, InferenceConfig())
+    pick = np.sort(np.random.default_rng(123).choice(4096, 96, replace=False))
+    sub = make_feature_batch(16384, np.asfortranarray(inputs.data[:, pick]),
+                             categories=pick, total_inputs=4096)
+    ref = oracle.infer(model, sub, threads=os.cpu_count() or 1)
+    got = np.intersect1d(res.categories, pick)
+    assert got.tolist() == ref.categories.tolist()
+    assert 0 < len(got) < len(pick)  # partial survival at density = |bias|
+    pos = np.searchsorted(res.categories, ref.categories)
+    assert same_bits(np.asarray(res.final.data)[:, pos], ref.final)
