@@ -381,7 +381,7 @@ template <int R, bool FMA, int FPL>
 __device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int *rows,
                                          const float *bias, int t, int lane, int M,
                                          uint32_t *s_alive) {
-  constexpr int T = Geo<FPL>::kTileF, LPW = 32 / FPL;  // lanes per 32-feature mask word
+  constexpr int T = Geo<FPL>::kTileF;
   const int j0 = t * T + FPL * lane;
   const int valid = M - j0;  // features of this lane that exist (may be <= 0)
   bool tiny = false;
@@ -389,12 +389,11 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int
                           ? finish_rows<R, FMA, FPL, true>(A, acc, rows, bias, j0, valid, tiny)
                           : finish_rows<R, FMA, FPL, false>(A, acc, rows, bias, j0, valid, tiny);
   if (FMA && tiny) atomicOr(A.guard, 1u);
-  // word w of the tile mask holds features 32w..32w+31 (lanes LPW*w .. LPW*w+LPW-1)
-  const uint32_t mine = am << (FPL * (lane % LPW));
+  // activity masks, q-major: word q bit l <=> feature FPL*l + q of the tile
 #pragma unroll
-  for (int w = 0; w < FPL; w++) {
-    const uint32_t word = __reduce_or_sync(0xffffffffu, lane / LPW == w ? mine : 0u);
-    if (lane == 0 && word) atomicOr(&s_alive[w], word);
+  for (int q = 0; q < FPL; q++) {
+    const uint32_t word = __ballot_sync(0xffffffffu, (am >> q) & 1u);
+    if (lane == 0 && word) atomicOr(&s_alive[q], word);
   }
 }
 
@@ -605,10 +604,12 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
   // <= nbuf apart, so the slot's barrier may still be one phase behind: the
   // header's entry number tells a stale phase from the awaited one.
   const u64 negz2 = pack2(A.negz, A.negz);
-  for (int u = warp;; u += C) {
-    const int k = u / gpi, g = u - k * gpi;
-    const int slot = k % nbuf;
-    const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
+  // unit u = warp + j*C  ->  (entry k, group g, ring slot, phase), advanced
+  // incrementally (no per-unit integer division)
+  int k = warp / gpi, g = warp - (warp / gpi) * gpi;
+  int slot = k % nbuf;
+  uint32_t phase = (uint32_t)(k / nbuf) & 1u;
+  for (;; ) {
     const char *buf = smem + slot * A.buf_bytes;
     const volatile Header *vh = reinterpret_cast<const volatile Header *>(buf);
     if (A.simple_wait) {
@@ -679,30 +680,39 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
         }
         if (lane == 0) A.tile_done[h.t] = 0;
         uint32_t mw[FPL];
-        int cnt[FPL], tot = 0;
+        int tot = 0, below = 0;
 #pragma unroll
-        for (int w = 0; w < FPL; w++) {
-          mw[w] = __shfl_sync(0xffffffffu, wv, w);
-          cnt[w] = __popc(mw[w]);
-          tot += cnt[w];
+        for (int q = 0; q < FPL; q++) {
+          mw[q] = __shfl_sync(0xffffffffu, wv, q);
+          tot += __popc(mw[q]);
+          below += __popc(mw[q] & ((1u << lane) - 1u));  // alive features of lanes < this
         }
         int base = 0;
         if (lane == 0 && tot) base = atomicAdd(A.m_out, tot);
         base = __shfl_sync(0xffffffffu, base, 0);
-        int pre = 0;
+        // this lane's features FPL*lane + q, in feature order
+        int rank = base + below;
 #pragma unroll
-        for (int w = 0; w < FPL; w++) {
-          if ((mw[w] >> lane) & 1u) {
-            const int rank = pre + __popc(mw[w] & ((1u << lane) - 1u));
-            const int j = h.t * T + 32 * w + lane;
-            A.a_out[base + rank] = j;
-            A.cat_out[base + rank] = A.cat_in[j];
+        for (int q = 0; q < FPL; q++) {
+          if ((mw[q] >> lane) & 1u) {
+            const int j = h.t * T + FPL * lane + q;
+            A.a_out[rank] = j;
+            A.cat_out[rank] = A.cat_in[j];
+            rank++;
           }
-          pre += cnt[w];
         }
       }
     }
     if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+    g += C;
+    while (g >= gpi) {
+      g -= gpi;
+      k++;
+      if (++slot == nbuf) {
+        slot = 0;
+        phase ^= 1u;
+      }
+    }
   }
 }
 
