@@ -111,7 +111,9 @@ int spdnn_plan_sizes(const spdnn_plan *plan, spdnn_plan_sizes_t *sizes);
  *   meta    int32[num_meta]: per block, 16-byte aligned:
  *           fp_cnt input neurons (smem slot order), pad to 4,
  *           ng x {record offset relative to rec_off, record count},
- *           ng x R output neurons (-1 = padding row), pad to 4
+ *           ng x R output neurons (-1 = padding row),
+ *           ng x R bias slots (fp32 bits; 0 from the builder, bias[row] once
+ *           the model is on the device -- filled by the host layer), pad to 4
  *   records uint32[num_records * record_words]
  *           word 0 = smem byte offset of the input neuron's staged row
  *           (slot * SPDNN_STAGED_ROW_BYTES), words 1..R = fp32 weight bits

@@ -334,10 +334,17 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
                                                 const float *bias, int j0, int valid,
                                                 bool &tiny) {
   constexpr int H = FPL / 2;
+  // FMA form (finite values guaranteed, else the run is redone): per feature the
+  // running unsigned min of bits(v) - 1 gives both tests: v > 0 exists <=> the
+  // min is not 0xffffffff, and a v in (0, tiny) exists <=> min < bits(tiny) - 1.
+  // Exact form: NaN may occur (non-finite inputs), alive uses a float max.
   float mx[FPL];
-  uint32_t mn = 0xffffffffu;  // min over outputs of bits(v) - 1: v in (0, tiny) check
+  uint32_t mn[FPL];
 #pragma unroll
-  for (int q = 0; q < FPL; q++) mx[q] = 0.0f;
+  for (int q = 0; q < FPL; q++) {
+    mx[q] = 0.0f;
+    mn[q] = 0xffffffffu;
+  }
 #pragma unroll
   for (int k = 0; k < R; k++) {
     const float2 b2 = make_float2(bias[k], bias[k]);
@@ -351,15 +358,13 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
   }
 #pragma unroll
   for (int k = 0; k < R; k++) {
-    if (rows[k] < 0) continue;
     const float *x = reinterpret_cast<const float *>(&acc[H * k]);
 #pragma unroll
     for (int q = 0; q < FPL; q++) {
-      if (FULL || q < valid) {
-        mx[q] = fmaxf(mx[q], x[q]);
-        if (FMA) mn = min(mn, __float_as_uint(x[q]) - 1u);
-      }
+      if (FMA) mn[q] = min(mn[q], __float_as_uint(x[q]) - 1u);  // padding rows give 0 -> no-op
+      else if (rows[k] >= 0) mx[q] = fmaxf(mx[q], x[q]);
     }
+    if (rows[k] < 0) continue;
     float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
     if (FULL) {
       if (FPL == 4) *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
@@ -370,12 +375,21 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
         if (q < valid) dst[q] = x[q];
     }
   }
-  if (FMA) tiny = mn < A.tiny_bits_m1;
-  uint32_t am = 0;
+  uint32_t am = 0, lo = 0xffffffffu;
 #pragma unroll
-  for (int q = 0; q < FPL; q++) am |= mx[q] > 0.0f ? (1u << q) : 0u;
+  for (int q = 0; q < FPL; q++) {
+    const bool in = FULL || q < valid;
+    if (FMA) {
+      am |= (in && mn[q] != 0xffffffffu) ? (1u << q) : 0u;
+      if (in) lo = min(lo, mn[q]);
+    } else {
+      am |= (in && mx[q] > 0.0f) ? (1u << q) : 0u;
+    }
+  }
+  if (FMA) tiny = lo < A.tiny_bits_m1;
   return am;
 }
+
 
 template <int R, bool FMA, int FPL>
 __device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int *rows,
@@ -540,7 +554,7 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
       const uint32_t smeta = buf + kHeaderBytes;
       const uint32_t srec = smeta + A.meta_bytes;
       const uint32_t sy = srec + A.rec_bytes;
-      const int meta_words = ((fp_cnt + 3) & ~3) + ((2 * ng + R * ng + 3) & ~3);
+      const int meta_words = ((fp_cnt + 3) & ~3) + ((2 * ng + 2 * R * ng + 3) & ~3);
       const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
       const int quads = (fp_cnt + 3) >> 2;
       if (ptid == 0) {
@@ -632,10 +646,11 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
       int rows[R];
       float bias[R];
       const int *mrows = meta + seg_base + 2 * h.ng + R * g;
+      const float *mbias = reinterpret_cast<const float *>(meta + seg_base + 2 * h.ng + R * h.ng) + R * g;
 #pragma unroll
       for (int r = 0; r < R; r++) {
         rows[r] = mrows[r];
-        bias[r] = rows[r] >= 0 ? __ldg(A.bias + rows[r]) : 0.0f;
+        bias[r] = mbias[r];  // bias[row] staged with the block metadata
       }
       u64 acc[H * R];
 #pragma unroll

@@ -187,7 +187,8 @@ void pad4(std::vector<int32_t> &v) {
 
 // Lay the groups out as blocks. Per block (include/spdnn_b200.h):
 //   descriptor {g_first, ng, nst, first_extra_stage, meta_off, fp_cnt, rec_off, rec_cnt}
-//   meta       [fp indices of stage 0][pad][ng x (rec_rel, cnt)][ng x R rows][pad]
+//   meta       [fp indices of stage 0][pad][ng x (rec_rel, cnt)][ng x R rows]
+//              [ng x R bias slots][pad]
 //   records    per group, its union columns in ascending order
 // A block with more than one stage holds exactly one group; its stages 1..
 // live in `stages` as {meta_off, fp_cnt, rec_off, rec_cnt} (meta = fp list).
@@ -278,6 +279,9 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
     pl->meta.insert(pl->meta.end(), gseg.begin(), gseg.end());
     for (size_t gg = g0; gg < g0 + ng; gg++)
       for (int k = 0; k < R; k++) pl->meta.push_back(gs[gg].rows[k]);
+    // bias slots, one per group row: zero here, filled with bias[row] when the
+    // model is uploaded (the layout does not depend on the bias values)
+    pl->meta.insert(pl->meta.end(), (size_t)R * ng, 0);
     pad4(pl->meta);
     pl->max_meta = std::max<int32_t>(pl->max_meta, (int32_t)(pl->meta.size() - meta_off));
     const int64_t first_extra = (int64_t)pl->stages.size() / 4;

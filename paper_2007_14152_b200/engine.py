@@ -233,6 +233,24 @@ def _stream_ptr(torch) -> ctypes.c_void_p:
     return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _fill_bias_slots(plan: "LayerPlan", meta: np.ndarray, bias: np.ndarray) -> np.ndarray:
+    """Copy of a plan's meta with every block's bias slots set to bias[row]
+    (0 for padding rows), so the kernel reads row biases from shared memory."""
+    meta = meta.copy()
+    R = plan.rows_per_group
+    blk = plan.blocks.reshape(-1, 8)
+    if blk.shape[0] == 0:
+        return meta
+    ng = blk[:, 1].astype(np.int64)
+    rows_at = blk[:, 4].astype(np.int64) + ((blk[:, 5].astype(np.int64) + 3) & ~3) + 2 * ng
+    cnt = R * ng
+    idx = np.repeat(rows_at - np.cumsum(cnt) + cnt, cnt) + np.arange(int(cnt.sum()))
+    rows = meta[idx]
+    vals = np.where(rows >= 0, bias[np.clip(rows, 0, None)], np.float32(0)).astype(np.float32)
+    meta[idx + np.repeat(cnt, cnt)] = vals.view(np.int32)
+    return meta
+
+
 class DeviceNetwork:
     """All layer plans of a network resident in HBM, plus the bias vector.
 
@@ -251,11 +269,14 @@ class DeviceNetwork:
         kinds = ("blocks", "stages", "meta", "records")
         self.buffers = {}
         offsets = {k: [] for k in kinds}
+        bias32 = np.ascontiguousarray(bias, np.float32)
         for k in kinds:
             parts = []
             off = 0
             for pl in plans:
                 a = getattr(pl, k)
+                if k == "meta":
+                    a = _fill_bias_slots(pl, a, bias32)
                 pad = (-a.shape[0] * a.itemsize) % 32  # every layer's slice 32-byte aligned
                 parts.append(a)
                 if pad:
