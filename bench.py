@@ -223,8 +223,12 @@ def run_ours_multi(args, cfg):
     from paper_2007_14152_b200.model import FeatureBatch, InferenceConfig, count_edges
 
     rank, world, local = dist_env()
+    # one rank per GPU over NCCL; SPDNN_DIST_BACKEND=gloo lets several ranks
+    # share one GPU (test boxes with a single device)
+    backend = os.environ.get("SPDNN_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", init_method="env://")
+    dist.init_process_group(backend, init_method="env://")
     dev = torch.device("cuda", local)
     model, inputs = build_workload(cfg)
     n, L = model.neurons, model.num_layers
@@ -496,7 +500,7 @@ def main():
     ap.add_argument("--plan", default="", help="layout knobs, e.g. max_groups=8,footprint_cap=96")
     ap.add_argument("--cpu-sample", type=int, default=1024,
                     help="inputs in the CPU-baseline sample (0 = skip the CPU leg)")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="grow the CPU sample to about this much CPU time (0 = fixed sample)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
