@@ -324,7 +324,7 @@ class DeviceNetwork:
 class Workspace:
     """Per-inference device buffers for a feature-count capacity (reused)."""
 
-    def __init__(self, neurons: int, m_cap: int, num_layers: int, device):
+    def __init__(self, neurons: int, m_cap: int, num_layers: int, device, buffers: int = 2):
         torch = _torch()
         self.neurons = neurons
         self.m_cap = m_cap
@@ -332,9 +332,10 @@ class Workspace:
         self.num_layers = num_layers
         f32, i32, i64 = torch.float32, torch.int32, torch.int64
         self.x = torch.empty((m_cap, neurons), dtype=f32, device=device)  # raw upload
-        self.y = [torch.empty((neurons, self.ld), dtype=f32, device=device) for _ in range(2)]
-        self.a = [torch.empty(self.ld, dtype=i32, device=device) for _ in range(2)]
-        self.cat = [torch.empty(self.ld, dtype=i64, device=device) for _ in range(2)]
+        nb = range(buffers)
+        self.y = [torch.empty((neurons, self.ld), dtype=f32, device=device) for _ in nb]
+        self.a = [torch.empty(self.ld, dtype=i32, device=device) for _ in nb]
+        self.cat = [torch.empty(self.ld, dtype=i64, device=device) for _ in nb]
         self.counts = torch.zeros(num_layers + 1, dtype=i32, device=device)
         self.tile_done = torch.zeros(self.ld // 64, dtype=i32, device=device)
         self.tile_alive = torch.zeros(self.ld // 32, dtype=i32, device=device)

@@ -21,9 +21,10 @@ functions and match the reference exactly:
 * ``gather_categories``<- parallel.py:238-245
 * ``run_batch_parallel`` <- parallel.py:379-454 (per-layer loop :294-376)
 
-The layer step itself is the sm_100a kernel (engine.py / csrc/layer.cu); the
-loop needs one device->host read of the survivor count per layer to drive the
-exchange, as the reference's barrier does.
+The layer step itself is the sm_100a kernel (engine.py / csrc/layer.cu). The
+reference's per-layer barrier becomes a speculative window of layers with one
+count allgather and one host read per window (run_layers_parallel), rewound
+and replayed up to the layer where the reference would rebalance.
 """
 
 from __future__ import annotations
@@ -245,49 +246,116 @@ def gather_categories(partition: Partition) -> list:
 
 class DeviceShard:
     """One worker's features on a GPU: the engine's workspace plus the
-    operations the exchange needs (count, take highest categories, append)."""
+    operations the runner and the exchange need.
 
-    def __init__(self, net, neurons: int, m_cap: int, num_layers: int):
+    Layers run in speculative *windows* (see run_layers_parallel): the state
+    at the start of a window stays untouched in its buffer (the checkpoint)
+    while the window's layers rotate through the two other buffers, so a
+    window can be rewound and replayed without copying any feature data.
+    """
+
+    BUFFERS = 3
+
+    def __init__(self, net, neurons: int, m_cap: int, num_layers: int, unpadded=None):
         from . import engine
         self.engine = engine
         self.net = net
         self.n = neurons
+        self.num_layers = num_layers
+        self.unpadded = unpadded  # () -> DeviceNetwork without zero-weight slots
         # receivers append after the columns in use: room for two full shards
         self.ws = engine.Workspace(neurons, 2 * max(m_cap, 1), num_layers,
-                                   net.bias.device)
+                                   net.bias.device, buffers=self.BUFFERS)
         self.cur = 0     # buffer holding the current active features
         self.m = 0       # active features (host mirror of the device count)
         self.used = 0    # columns of ws.y[cur] in use (appends go after them)
+        self.fma = None  # None: the network's default form; False: exact form
+        self.unpadded_active = False
+        self._win = None
 
     def load(self, x_rows, categories) -> None:
-        """x_rows: (M, N) feature-major host or device tensor."""
+        """x_rows: (M, N) feature-major host or device tensor. Resets the
+        guard flags (stage_inputs screens the inputs for the FMA form)."""
         self.engine.stage_inputs(self.ws, x_rows, categories, self.net)
         self.cur, self.m, self.used = 0, int(x_rows.shape[0]), int(x_rows.shape[0])
+        self.fma = None
 
-    def step(self, l: int, fma: bool | None = None) -> None:
-        """Enqueue layer l on the current stream (engine.run_layers, one layer)."""
+    # -- windows ----------------------------------------------------------
+    def begin_window(self, l0: int, k: int) -> None:
+        """Enqueue layers l0..l0+k-1 from the current state (no host sync)."""
+        self._win = (l0, k, self.cur, self.m, self.used)
+        self._enqueue(l0, k)
+
+    def _enqueue(self, l0: int, k: int) -> None:
         import ctypes
         from . import _native
-        e, ws = self.engine, self.ws
-        i, o = self.cur, self.cur ^ 1
-        ws.counts[l] = self.m
-        ws.counts[l + 1] = 0
-        ws.work[l] = 0
-        opts = e.run_opts(self.net, fma)
+        e, ws, net = self.engine, self.ws, self.net
+        ck = self.cur
+        ws.counts[l0] = self.m
+        ws.counts[l0 + 1: l0 + k + 1].zero_()
+        ws.work[l0: l0 + k].zero_()
+        opts = e.run_opts(net, self.fma)
+        stream = e._stream_ptr(e._torch())
+        cnt = ws.counts.data_ptr()
+        o1, o2 = (ck + 1) % 3, (ck + 2) % 3
         _native.check(_native.lib().spdnn_layer_forward(
-            ctypes.byref(self.net.layer_devs[l]), e._dptr(self.net.bias), e._dptr(ws.y[i]),
-            e._dptr(ws.y[o]), ws.ld, e._dptr(ws.a[i]), e._dptr(ws.cat[i]),
-            ctypes.c_void_p(ws.counts.data_ptr() + 4 * l), e._dptr(ws.a[o]), e._dptr(ws.cat[o]),
-            ctypes.c_void_p(ws.counts.data_ptr() + 4 * (l + 1)), ctypes.byref(ws.scratch),
-            ctypes.c_void_p(ws.work.data_ptr() + 4 * l), ctypes.byref(opts),
-            e._stream_ptr(e._torch())), "spdnn_layer_forward")
-        self.used = self.m  # the output columns 0..m-1 of buffer o
-        self.cur = o
-        self.pending_layer = l
+            ctypes.byref(net.layer_devs[l0]), e._dptr(net.bias), e._dptr(ws.y[ck]),
+            e._dptr(ws.y[o1]), ws.ld, e._dptr(ws.a[ck]), e._dptr(ws.cat[ck]),
+            ctypes.c_void_p(cnt + 4 * l0), e._dptr(ws.a[o1]), e._dptr(ws.cat[o1]),
+            ctypes.c_void_p(cnt + 4 * (l0 + 1)), ctypes.byref(ws.scratch),
+            ctypes.c_void_p(ws.work.data_ptr() + 4 * l0), ctypes.byref(opts), stream),
+            "spdnn_layer_forward")
+        if k > 1:
+            # the rest of the window ping-pongs o1 <-> o2 inside one C call
+            sc = _native.Scratch(ws.tile_done.data_ptr(), ws.tile_alive.data_ptr(),
+                                 ws.work.data_ptr() + 4 * (l0 + 1), ws.guard.data_ptr())
+            devs = ctypes.c_void_p(ctypes.addressof(net.layer_devs)
+                                   + ctypes.sizeof(_native.LayerDev) * (l0 + 1))
+            _native.check(_native.lib().spdnn_infer_layers(
+                k - 1, devs, e._dptr(net.bias), e._dptr(ws.y[o1]), e._dptr(ws.y[o2]), ws.ld,
+                e._dptr(ws.a[o1]), e._dptr(ws.a[o2]), e._dptr(ws.cat[o1]), e._dptr(ws.cat[o2]),
+                ctypes.c_void_p(cnt + 4 * (l0 + 1)), ctypes.byref(sc), ctypes.byref(opts),
+                stream), "spdnn_infer_layers")
+        self._final = o1 if (k - 1) % 2 == 0 else o2
 
-    def sync_count(self) -> int:
-        self.m = int(self.ws.counts[self.pending_layer + 1].item())
-        return self.m
+    def window_counts(self):
+        """Device int64 [active after each window layer..., guard bits]."""
+        torch = self.engine._torch()
+        l0, k = self._win[0], self._win[1]
+        return torch.cat([self.ws.counts[l0 + 1: l0 + k + 1], self.ws.guard]).to(torch.int64)
+
+    def rewind(self) -> None:
+        """Back to the window's starting state (its buffer was never written)."""
+        self.cur, self.m, self.used = self._win[2], self._win[3], self._win[4]
+
+    def replay(self, k: int) -> None:
+        """Rewind and run only the first k layers of the window."""
+        l0 = self._win[0]
+        self.rewind()
+        self._win = (l0, k) + self._win[2:]
+        self._enqueue(l0, k)
+
+    def commit(self, m_last_in: int, m: int) -> None:
+        """Accept the window: its last output becomes the current state. The
+        kernel writes a feature's outputs at its input position, so the
+        columns in use are those of the last layer's input."""
+        self.cur = self._final
+        self.m, self.used = int(m), int(m_last_in)
+        self._win = None
+
+    def set_exact(self, unpadded: bool) -> None:
+        """Switch to the exact arithmetic form (guard fired); with non-finite
+        inputs also to plans without zero-weight union slots."""
+        self.fma = False
+        if unpadded:
+            if self.unpadded is None:
+                raise ModelError("non-finite inputs need the unpadded plans")
+            self.net = self.unpadded()
+            self.unpadded_active = True
+
+    @property
+    def uses_fma(self) -> bool:
+        return bool(self.engine.run_opts(self.net, self.fma).fma_form)
 
     def take_top(self, k: int):
         """Remove the k highest-category active features; returns their values
@@ -367,6 +435,11 @@ class LocalTransport:
                         self.hook(CountMsg(src=w, layer=layer, count=mine[w]))
         return [mine[w] for w in range(self.workers)]
 
+    def allgather_window(self, mine: dict) -> np.ndarray:
+        """(workers, k+1) host array of every worker's window counts + guard."""
+        import torch
+        return torch.stack([mine[w] for w in range(self.workers)]).cpu().numpy()
+
     def exchange(self, layer: int, plan: TransferPlan, shards: dict) -> None:
         incoming = {w: [] for w in range(self.workers)}
         for src, dst, k in plan:
@@ -424,6 +497,15 @@ class DistTransport:
                     self.hook(CountMsg(src=self.rank, layer=layer, count=mine[self.rank]))
         return [int(v.item()) for v in out]
 
+    def allgather_window(self, mine: dict) -> np.ndarray:
+        """One allgather of the window's counts (device-resident under NCCL)
+        and one host read for the whole window."""
+        import torch
+        t = self._wire(mine[self.rank].contiguous())
+        out = [self._empty(t.shape[0], torch.int64) for _ in range(self.workers)]
+        self.dist.all_gather(out, t)
+        return torch.stack(out).cpu().numpy()
+
     def exchange(self, layer: int, plan: TransferPlan, shards: dict) -> None:
         import torch
         me = shards[self.rank]
@@ -471,50 +553,100 @@ class DistTransport:
 # ---------------------------------------------------------------------------
 # the runner
 
+WINDOW_MIN = 4
+WINDOW_MAX = int(__import__("os").environ.get("SPDNN_WINDOW_MAX", "64"))
+
+
 def run_layers_parallel(num_layers: int, shards: dict, transport, threshold: float,
-                        workers: int, step=None, values: bool = True):
+                        workers: int, values: bool = True, window: int | None = None):
     """Per-layer loop of parallel.py:294-376 over any shard/transport pair.
 
-    ``step(shard, l)`` runs layer l on one shard and returns its new count
-    (default: the device kernel + one count read). Returns (per-layer
-    outcomes as (before_total, after_total) pairs, CommMatrix, BalanceReport,
-    gathered parts).
+    The reference synchronises every worker after every layer to exchange
+    survivor counts. Here the layers run in speculative windows of k layers
+    with no host synchronisation inside: each shard enqueues k layers, one
+    allgather moves all k counts (plus the arithmetic guard bits), and the
+    host then replays the reference's per-layer decisions over them. If layer
+    j of the window would have triggered a rebalance (or the all-dead stop),
+    every shard rewinds to the window's start and runs only layers ..j, then
+    the exchange happens exactly where the reference does it. Windows grow
+    from WINDOW_MIN to WINDOW_MAX while no rebalance occurs. The per-layer
+    counts, transfer plans, CommMatrix and BalanceReport are therefore those
+    of the per-layer loop.
+
+    A guard bit (FMA-form underflow risk or non-finite inputs, see engine)
+    on any worker rewinds the window and reruns it in the exact form.
+
+    Returns (per-layer (before_total, after_total) pairs, CommMatrix,
+    BalanceReport, gathered parts).
     """
     comm = CommMatrix.zeros(workers)
     balance = BalanceReport()
     totals = []
-    before = sum(transport.allgather_counts(-1, {w: shards[w].m for w in transport.local}))
-    for l in range(num_layers):
+    hook = transport.hook
+    local = transport.local
+    before = sum(transport.allgather_counts(-1, {w: shards[w].m for w in local}))
+    k_max = max(1, window or WINDOW_MAX)
+    k_cur = min(WINDOW_MIN, k_max)
+    l = 0
+    while l < num_layers:
         if before == 0:
-            totals.append((0, 0))
-            continue
-        mine = {}
-        for w in transport.local:
-            if step is None:
-                shards[w].step(l)
-        for w in transport.local:
-            mine[w] = shards[w].sync_count() if step is None else step(shards[w], l)
-        counts = transport.allgather_counts(l, mine)
-        totals.append((before, sum(counts)))
-        ratio = imbalance_ratio(counts)
-        plan = balance_step(counts) if ratio > threshold else []
-        if plan:
-            transport.exchange(l, plan, shards)
-        after = list(counts)
-        delta = np.zeros((workers, workers), dtype=np.int64)
-        for src, dst, k in plan:
-            after[src] -= k
-            after[dst] += k
-            delta[src, dst] += k
-        comm.add(delta)
-        balance.entries.append(BalanceEntry(
-            layer=l, before_counts=tuple(counts), after_counts=tuple(after),
-            imbalance_before=ratio, imbalance_after=imbalance_ratio(after),
-            moved_rows=sum(k for _, _, k in plan), rebalanced=bool(plan)))
-        before = sum(counts)
-        if before == 0:
-            totals.extend([(0, 0)] * (num_layers - l - 1))
+            totals.extend([(0, 0)] * (num_layers - l))
             break
+        k = min(k_cur, num_layers - l)
+        for w in local:
+            shards[w].begin_window(l, k)
+        hist = transport.allgather_window({w: shards[w].window_counts() for w in local})
+        guard = int(np.bitwise_or.reduce(hist[:, k]))
+        unpadded = bool(guard & 2)
+        if (guard & 1 and any(shards[w].uses_fma for w in local)) or \
+                (unpadded and not all(shards[w].unpadded_active for w in local)):
+            for w in local:
+                shards[w].rewind()
+                shards[w].set_exact(unpadded)
+            continue
+        accept, plan = k, []
+        for j in range(k):
+            counts = [int(c) for c in hist[:, j]]
+            if sum(counts) == 0:
+                accept = j + 1
+                break
+            if imbalance_ratio(counts) > threshold:
+                accept = j + 1
+                break
+        if accept < k:
+            for w in local:
+                shards[w].replay(accept)
+        for j in range(accept):
+            counts = [int(c) for c in hist[:, j]]
+            if hook is not None:
+                for w in local:
+                    for other in range(workers):
+                        if other != w:
+                            hook(CountMsg(src=w, layer=l + j, count=counts[w]))
+            totals.append((before, sum(counts)))
+            ratio = imbalance_ratio(counts)
+            plan = balance_step(counts) if ratio > threshold else []
+            after = list(counts)
+            delta = np.zeros((workers, workers), dtype=np.int64)
+            for src, dst, n in plan:
+                after[src] -= n
+                after[dst] += n
+                delta[src, dst] += n
+            comm.add(delta)
+            balance.entries.append(BalanceEntry(
+                layer=l + j, before_counts=tuple(counts), after_counts=tuple(after),
+                imbalance_before=ratio, imbalance_after=imbalance_ratio(after),
+                moved_rows=sum(n for _, _, n in plan), rebalanced=bool(plan)))
+            before = sum(counts)
+        for w in local:
+            last_in = int(hist[w, accept - 2]) if accept > 1 else shards[w].m
+            shards[w].commit(last_in, int(hist[w, accept - 1]))
+        l += accept
+        if plan:
+            transport.exchange(l - 1, plan, shards)
+            k_cur = min(WINDOW_MIN, k_max)
+        else:
+            k_cur = min(2 * k_cur, k_max)
     parts = transport.gather(shards, values)
     return totals, comm, balance, parts
 
@@ -545,10 +677,17 @@ def run_batch_parallel(model: NetworkModel, inputs: FeatureBatch, config: Infere
     m_cap = max((hi - lo for lo, hi in bounds), default=0)
     transport = DistTransport(latency_hook, dev) if distributed else \
         LocalTransport(w, latency_hook)
+    cache = []
+
+    def unpadded():
+        if not cache:
+            cache.append(engine.DeviceNetwork(engine._unpadded(prepared, model), model.bias))
+        return cache[0]
+
     shards = {}
     for r in transport.local:
         lo, hi = bounds[r]
-        sh = DeviceShard(net, model.neurons, m_cap, model.num_layers)
+        sh = DeviceShard(net, model.neurons, m_cap, model.num_layers, unpadded=unpadded)
         x = torch.from_numpy(np.ascontiguousarray(np.asarray(inputs.data)[:, lo:hi].T))
         sh.load(x, torch.from_numpy(np.ascontiguousarray(inputs.categories[lo:hi])))
         shards[r] = sh

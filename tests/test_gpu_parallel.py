@@ -154,3 +154,38 @@ def test_distributed_transport_two_ranks(cuda_ok):
         assert per_layer == [(o.active_before, o.active_after) for o in single.per_layer]
         assert vsum == float(np.asarray(single.final.data, np.float64).sum())
     assert res[0][1:] == res[1][1:]
+
+
+def test_stress_matches_reference_run_batch_parallel(cuda_ok):
+    """Skewed shards (C5 recipe) through DeviceShards + speculative windows:
+    categories, per-layer totals, every BalanceEntry, the CommMatrix and the
+    final values equal the reference's run_batch_parallel (stress.json)."""
+    from test_parallel_host import _check_stress, _stress_cases, _stress_problem
+    for case in _stress_cases():
+        model, inputs, thr = _stress_problem(case)
+        res, comm, bal = parallel.run_batch_parallel(
+            model, inputs, InferenceConfig(workers=case["workers"], rebalance_threshold=thr))
+        _check_stress(case, [(o.active_before, o.active_after) for o in res.per_layer],
+                      comm, bal, res.categories.tolist(), np.asarray(res.final.data).T)
+
+
+@pytest.mark.parametrize("poison", ["tiny", "nan"])
+def test_guard_rewinds_windows(cuda_ok, poison):
+    """Inputs that break the FMA form's exactness (subnormal-range values) or
+    poison the union padding (NaN): the window is rewound and rerun in the
+    exact form / unpadded plans, matching the single-worker engine."""
+    model, inputs = _edge(m=300)
+    data = np.asarray(inputs.data).copy()
+    if poison == "tiny":
+        data[:7, 200:220] = np.float32(3e-39)
+    else:
+        data[5, 150] = np.nan
+    inputs = make_feature_batch(1024, data)
+    cfg = InferenceConfig(workers=3, rebalance_threshold=1.05)
+    res, comm, bal = parallel.run_batch_parallel(model, inputs, cfg)
+    single = engine.infer(model, inputs, InferenceConfig())
+    assert np.array_equal(res.categories, single.categories)
+    assert np.array_equal(np.asarray(res.final.data).view(np.uint32),
+                          np.asarray(single.final.data).view(np.uint32))
+    ref = oracle.infer(model, inputs)
+    assert res.categories.tolist() == ref.categories.tolist()

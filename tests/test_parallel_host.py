@@ -100,8 +100,7 @@ def test_local_exchange_loop_rebalances():
     model, inputs = _problem()
     shards = _shards(model, inputs, 2, [0, 1])
     totals, comm, bal, parts = run_layers_parallel(
-        model.num_layers, shards, LocalTransport(2, None), 1.25, 2,
-        step=lambda sh, l: sh.step(l))
+        model.num_layers, shards, LocalTransport(2, None), 1.25, 2)
     cats = np.sort(torch.cat([p[0] for p in parts]).numpy())
     ref = oracle.infer(model, inputs)
     assert cats.tolist() == ref.categories.tolist()
@@ -125,7 +124,7 @@ def _gloo_worker(rank, world, port, q):
         shards = _shards(model, inputs, world, [rank])
         t = DistTransport(None, torch.device("cpu"))
         totals, comm, bal, parts = run_layers_parallel(
-            model.num_layers, shards, t, 1.25, world, step=lambda sh, l: sh.step(l))
+            model.num_layers, shards, t, 1.25, world)
         cats = np.sort(torch.cat([p[0] for p in parts]).numpy())
         vals = torch.cat([p[1] for p in parts]).numpy()
         q.put((rank, cats.tolist(), [b for b, _ in totals], comm.matrix.tolist(),
@@ -153,3 +152,91 @@ def test_gloo_world_size_2_exchange():
         assert any(rebalanced) and matrix[0][1] > 0
         assert vsum == pytest.approx(float(np.asarray(ref.final).sum()))
     assert res[0][1:] == res[1][1:]  # every rank returns the same merged answer
+
+
+# ---------------------------------------------------------------------------
+# skewed shards (config C5's recipe) against the reference's own
+# run_batch_parallel (tests/golden/stress.json, made by make_stress.py)
+
+def _stress_cases():
+    return json.load(open(os.path.join(GOLDEN, "stress.json")))
+
+
+def _stress_problem(case):
+    n, w, cols, bias = case["neurons"], case["workers"], case["columns"], case["bias"]
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=n, layers=case["layers"], connections_per_neuron=32, bias_value=bias, seed=1))
+    parts = [ingest.generate_synthetic_inputs(n, cols, abs(bias) + 0.04 - 0.01 * s,
+                                              seed=100 + s) for s in range(w)]
+    data = np.concatenate([np.asarray(p.data) for p in parts], axis=1)
+    thr = math.inf if case["threshold"] == "inf" else case["threshold"]
+    return model, make_feature_batch(n, data), thr
+
+
+def _check_stress(case, totals, comm, bal, cats, final=None):
+    assert cats == case["categories"]
+    assert [list(t) for t in totals] == case["per_layer"]
+    got = [[e.layer, list(e.before_counts), list(e.after_counts), e.moved_rows,
+            bool(e.rebalanced)] for e in bal.entries]
+    assert got == case["entries"]
+    assert comm.matrix.tolist() == case["comm"]
+    if final is not None:
+        import hashlib
+        assert hashlib.sha256(np.ascontiguousarray(final, dtype="<f4").tobytes()
+                              ).hexdigest() == case["final_sha256"]
+
+
+@pytest.mark.parametrize("window", [None, 1, 3])
+def test_windowed_loop_matches_reference_stress(window):
+    """The speculative-window runner reproduces the reference's per-layer
+    decisions exactly (rebalances at the same layers, same plans) whatever
+    the window length."""
+    for case in _stress_cases():
+        model, inputs, thr = _stress_problem(case)
+        w = case["workers"]
+        shards = _shards(model, inputs, w, list(range(w)))
+        totals, comm, bal, parts = run_layers_parallel(
+            model.num_layers, shards, LocalTransport(w, None), thr, w, window=window)
+        cats = torch.cat([p[0] for p in parts]).numpy()
+        vals = torch.cat([p[1] for p in parts]).numpy()
+        order = np.argsort(cats, kind="stable")
+        _check_stress(case, totals, comm, bal, cats[order].tolist(), vals[order])
+        if window is None and bal.total_moved:
+            # windows were rewound at the rebalancing layers and regrown after
+            assert any(k > 4 for _, k in shards[0].windows)
+
+
+def _gloo_stress_worker(rank, world, port, q, idx):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        case = _stress_cases()[idx]
+        model, inputs, thr = _stress_problem(case)
+        shards = _shards(model, inputs, world, [rank])
+        t = DistTransport(None, torch.device("cpu"))
+        totals, comm, bal, parts = run_layers_parallel(model.num_layers, shards, t, thr, world)
+        cats = torch.cat([p[0] for p in parts]).numpy()
+        vals = torch.cat([p[1] for p in parts]).numpy()
+        order = np.argsort(cats, kind="stable")
+        _check_stress(case, totals, comm, bal, cats[order].tolist(), vals[order])
+        q.put((rank, "ok"))
+    except Exception as e:  # noqa: BLE001 - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world_size_3_stress():
+    idx = next(i for i, c in enumerate(_stress_cases()) if c["workers"] == 3)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_stress_worker, args=(r, 3, port, q, idx))
+             for r in range(3)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(3))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == [(0, "ok"), (1, "ok"), (2, "ok")]
