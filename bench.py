@@ -301,8 +301,8 @@ def run_ours_multi(args, cfg):
                          "peak": peak, "unit": "GB/s",
                          "frac": bytes_total / (ms / 1e3) / 1e9 / peak, "traffic": None,
                          "peak_source": peak_src,
-                         "note": "per-GPU algorithmic bytes over the whole step (host-synced "
-                                 "count exchange included)"},
+                         "note": "per-GPU algorithmic bytes over the whole step (count "
+                                 "exchange, one allgather per layer window, included)"},
             "cpu_baseline": None, "clocks": clocks.summary(),
             "gpu_launches": args.steps * L}), flush=True)
     dist.destroy_process_group()
@@ -315,7 +315,9 @@ def run_ours(args, cfg):
     from paper_2007_14152_b200.model import FeatureBatch, InferenceConfig, count_edges
 
     rank, world, local = dist_env()
-    if world > 1:
+    # SPDNN_BENCH_PARALLEL=1 times the batch-parallel runner even at N=1
+    # (its per-window overhead against the single-worker engine)
+    if world > 1 or os.environ.get("SPDNN_BENCH_PARALLEL") == "1":
         return run_ours_multi(args, cfg)
     dev = torch.device("cuda", torch.cuda.current_device())
     t0 = time.time()
