@@ -51,6 +51,12 @@ CONFIGS = {
                name="graph-challenge-synthetic 4096x480, bias -0.35 (BASELINE.json configs[1])"),
     "c3": dict(neurons=16384, layers=1920, bias=-0.40, density=0.40, inputs=60000,
                name="graph-challenge-synthetic 16384x1920, bias -0.4 (BASELINE.json configs[2])"),
+    "c4": dict(neurons=65536, layers=1920, bias=-0.45, density=0.45, inputs=60000, chunked=True,
+               name="graph-challenge-synthetic 65536x1920, bias -0.45 (BASELINE.json configs[3])"),
+    "c5": dict(neurons=16384, layers=1920, bias=-0.40, density=0.40, inputs=60000, stress=True,
+               workers=8,
+               name="load-imbalance stress: skewed shards on config 3's network, rebalancing "
+                    "on vs off (BASELINE.json configs[4])"),
 }
 K_CONN = 32
 MODEL_SEED, INPUT_SEED = 1, 2
@@ -180,11 +186,69 @@ def cpu_baseline(model, inputs, sample_cols: int, threads: int, target_s: float 
     return dict(value=edges / dt / 1e12, seconds=dt, counts=r.counts, sample_cols=sample_cols)
 
 
+def run_reference_streamed(args, cfg):
+    """C4's reference arm: the 32 GB network is generated layer by layer and
+    the oracle runs each layer on a fixed 32-column sample as it streams by
+    (only the oracle's time is counted); one pass = one step."""
+    from paper_2007_14152_b200 import ingest
+    spec = ingest.GeneratorSpec(neurons=cfg["neurons"], layers=cfg["layers"],
+                                connections_per_neuron=K_CONN, bias_value=cfg["bias"],
+                                seed=MODEL_SEED)
+    threads = os.cpu_count() or 1
+    cols = np.sort(np.random.default_rng(123).choice(cfg["inputs"], 32, replace=False))
+    full = _sample_columns(cfg, cols)
+    orc = StreamedOracle(full, np.arange(len(cols)), ingest.synthetic_bias(spec), threads)
+    nnz = 0
+    chunk = []
+    for lay in ingest.iter_synthetic_layers(spec):
+        nnz += lay.nnz
+        chunk.append(lay)
+        if len(chunk) == 16:
+            orc(0, chunk)
+            chunk = []
+    if chunk:
+        orc(0, chunk)
+    v = len(cols) * nnz / orc.seconds / 1e12
+    return v, orc.seconds, len(cols), threads, (
+        f"{len(cols)} fixed-seed columns of {cfg['inputs']} through all {cfg['layers']} "
+        f"layers, generated and run layer by layer (oracle/spdnn_oracle.c, {threads} threads, "
+        f"{orc.seconds:.1f} s of oracle time)")
+
+
+def _sample_columns(cfg, cols):
+    """Columns `cols` of the synthetic input stream without holding the batch."""
+    n, m = cfg["neurons"], cfg["inputs"]
+    rng = np.random.default_rng(INPUT_SEED)
+    out = np.empty((n, len(cols)), np.float32, order="F")
+    for r0 in range(0, n, 1024):
+        r1 = min(n, r0 + 1024)
+        out[r0:r1, :] = rng.random((r1 - r0, m))[:, cols] < cfg["density"]
+    return out
+
+
 def run_reference(args, cfg):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    model, inputs = build_workload(cfg)
+    if cfg.get("chunked"):
+        v, secs, sample, threads, what = run_reference_streamed(args, cfg)
+        print(json.dumps({
+            "metric": "TeraEdges/s", "impl": "reference", "value": v, "unit": "TE/s",
+            "n_gpus": world, "steps": 1, "warmup": 0, "ms_per_step": secs * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
+                       "input_density": cfg["density"], "sample_inputs": sample},
+            "cpu_baseline": {"value": v, "unit": "TE/s", "cores": threads, "kind": "port",
+                             "sample": what},
+            "e2e": {"value": v, "unit": "TE/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
+    if cfg.get("stress"):
+        model, _ = build_workload(dict(cfg, inputs=0))
+        inputs = stress_inputs(cfg)
+    else:
+        model, inputs = build_workload(cfg)
     threads = os.cpu_count() or 1
     sample = args.cpu_sample
     vals, secs = [], []
@@ -216,11 +280,13 @@ def run_ours_multi(args, cfg):
     """N > 1: the batch-parallel runner (parallel.py) over NCCL, one rank per
     GPU: per layer the survivor counts are allgathered, transfers planned and
     executed when max/min exceeds the threshold; categories gathered at the
-    end. Time = max over ranks of the CUDA-event span of K full inferences."""
+    end. Time = max over ranks of the CUDA-event span of K full inferences.
+    Each rank generates only its own shard of the inputs, and C4's network is
+    built chunk by chunk (DeviceNetwork.from_layers) on every rank."""
     import torch
     import torch.distributed as dist
-    from paper_2007_14152_b200 import engine, parallel
-    from paper_2007_14152_b200.model import FeatureBatch, InferenceConfig, count_edges
+    from paper_2007_14152_b200 import engine, ingest, parallel
+    from paper_2007_14152_b200.model import InferenceConfig
 
     rank, world, local = dist_env()
     # one rank per GPU over NCCL; SPDNN_DIST_BACKEND=gloo lets several ranks
@@ -230,15 +296,29 @@ def run_ours_multi(args, cfg):
     torch.cuda.set_device(local)
     dist.init_process_group(backend, init_method="env://")
     dev = torch.device("cuda", local)
-    model, inputs = build_workload(cfg)
-    n, L = model.neurons, model.num_layers
-    lo, hi = parallel.shard_bounds(inputs.active_count, world)[rank]
-    m_cap = max(b - a for a, b in parallel.shard_bounds(inputs.active_count, world))
-    prepared = engine.prepare_model(model, InferenceConfig(), "optimized")
-    net = engine.device_network(prepared, model.bias)
-    shard = parallel.DeviceShard(net, n, m_cap, L)
-    x_dev = torch.from_numpy(np.ascontiguousarray(np.asarray(inputs.data)[:, lo:hi].T)).to(dev)
-    c_dev = torch.from_numpy(np.ascontiguousarray(inputs.categories[lo:hi])).to(dev)
+    n, total = cfg["neurons"], cfg["inputs"]
+    spec = ingest.GeneratorSpec(neurons=n, layers=cfg["layers"], connections_per_neuron=K_CONN,
+                                bias_value=cfg["bias"], seed=MODEL_SEED)
+    bounds = parallel.shard_bounds(total, world)
+    lo, hi = bounds[rank]
+    m_cap = max(b - a for a, b in bounds)
+    pinned = torch.empty((hi - lo, n), dtype=torch.float32).pin_memory()
+    shard_batch = ingest.generate_synthetic_inputs(n, total, cfg["density"], seed=INPUT_SEED,
+                                                   out=pinned.numpy().T, columns=(lo, hi))
+    if cfg.get("chunked"):
+        net = engine.DeviceNetwork.from_layers(ingest.iter_synthetic_layers(spec),
+                                               ingest.synthetic_bias(spec), chunk=64)
+        unpadded = None
+    else:
+        model = ingest.generate_synthetic_network(spec)
+        prepared = engine.prepare_model(model, InferenceConfig(), "optimized")
+        net = engine.device_network(prepared, model.bias)
+        unpadded = lambda: engine.DeviceNetwork(engine._unpadded(prepared, model), model.bias)
+    L = net.num_layers
+    edges_per_input = int(sum(net.nnz))
+    shard = parallel.DeviceShard(net, n, m_cap, L, unpadded=unpadded)
+    x_dev = pinned.to(dev)
+    c_dev = torch.from_numpy(np.ascontiguousarray(shard_batch.categories)).to(dev)
     transport = parallel.DistTransport(None, dev)
     thr = InferenceConfig().rebalance_threshold
 
@@ -264,19 +344,21 @@ def run_ours_multi(args, cfg):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     totals, comm, bal, parts = out
-    edges = cfg["inputs"] * count_edges(model)
+    edges = total * edges_per_input
     value = edges / (ms / 1e3) / 1e12
     sum_active = sum(b for b, _ in totals)
-    bytes_total = sum(8.0 * n * b + 6.0 * lay.nnz + 4.0 * n
-                      for (b, _), lay in zip(totals, model.layers) if b) / world
+    bytes_total = sum(8.0 * n * b + 6.0 * nz + 4.0 * n
+                      for (b, _), nz in zip(totals, net.nnz) if b) / world
     peak, peak_src = measured_peaks()
     ratios = [e.imbalance_before for e in bal.entries]
-    # e2e: the public API with host inputs (each rank uploads its shard)
+    del x_dev
+    # e2e: the public API with host inputs (each rank uploads its own shard)
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
-    res, _, _ = parallel.run_batch_parallel(model, inputs, InferenceConfig(workers=world),
-                                            prepared=prepared, values=False)
+    res, _, _ = parallel.run_batch_parallel_device(
+        net, shard_batch, InferenceConfig(workers=world), values=False,
+        edges_per_input=edges_per_input, unpadded=unpadded, shard_only=True)
     torch.cuda.synchronize()
     e2e = torch.tensor([time.perf_counter() - t0], device=dev)
     dist.all_reduce(e2e, op=dist.ReduceOp.MAX)
@@ -286,7 +368,7 @@ def run_ours_multi(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
+            "config": {"workload": cfg["name"], "inputs": total,
                        "input_density": cfg["density"], "survivors": int(len(res.categories)),
                        "sum_active": int(sum_active), "parallelism": f"batch-parallel x{world}",
                        "l2": "inputs larger than L2",
@@ -296,7 +378,7 @@ def run_ours_multi(args, cfg):
             "e2e": {"value": edges / float(e2e.item()) / 1e12, "unit": "TE/s",
                     "h2d_bytes_per_step": (hi - lo) * n * 4 + (hi - lo) * 8,
                     "d2h_bytes_per_step": int(len(res.categories)) * 8,
-                    "path": "parallel.run_batch_parallel(values=False)"},
+                    "path": "parallel.run_batch_parallel_device(values=False, shard_only=True)"},
             "roofline": {"bound": "hbm", "achieved": bytes_total / (ms / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s",
                          "frac": bytes_total / (ms / 1e3) / 1e9 / peak, "traffic": None,
@@ -308,45 +390,172 @@ def run_ours_multi(args, cfg):
     dist.destroy_process_group()
 
 
+class Workload:
+    """What the single-GPU timing loop needs, however the network was built."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def pinned_inputs(cfg):
+    """The synthetic batch generated straight into pinned host memory: the
+    e2e leg uploads from it and the device-resident copy is made once."""
+    import torch
+    from paper_2007_14152_b200 import ingest
+    n, m = cfg["neurons"], cfg["inputs"]
+    pinned = torch.empty((m, n), dtype=torch.float32).pin_memory()
+    batch = ingest.generate_synthetic_inputs(n, m, cfg["density"], seed=INPUT_SEED,
+                                             out=pinned.numpy().T)
+    return pinned, batch
+
+
+def resident_workload(args, cfg, params):
+    """C1-C3: the whole model on the host, prepared once (engine.prepare_model)."""
+    from paper_2007_14152_b200 import engine, ingest
+    from paper_2007_14152_b200.model import InferenceConfig
+    spec = ingest.GeneratorSpec(neurons=cfg["neurons"], layers=cfg["layers"],
+                                connections_per_neuron=K_CONN, bias_value=cfg["bias"],
+                                seed=MODEL_SEED)
+    model = ingest.generate_synthetic_network(spec)
+    t0 = time.time()
+    prepared = engine.prepare_model(model, InferenceConfig(), "optimized", params=params)
+    net = engine.device_network(prepared, model.bias)
+    log(f"prepared+uploaded {model.num_layers} layers in {time.time() - t0:.1f}s "
+        f"({net.hbm_bytes / 1e6:.0f} MB of layout)")
+
+    def e2e(batch):
+        return engine.infer(model, batch, InferenceConfig(), prepared=prepared, values=False)
+
+    def cpu(inputs):
+        threads = os.cpu_count() or 1
+        r = cpu_baseline(model, inputs, args.cpu_sample, threads, target_s=args.cpu_seconds)
+        return {"value": r["value"], "unit": "TE/s", "cores": threads, "kind": "port",
+                "sample": f"first {r['sample_cols']} of {cfg['inputs']} inputs, all "
+                          f"{model.num_layers} layers, oracle/spdnn_oracle.c on {threads} "
+                          f"host threads ({r['seconds']:.1f} s)"}
+
+    return Workload(net=net, nnz=np.array([l.nnz for l in model.layers], np.float64),
+                    e2e=e2e, e2e_path="engine.infer(values=False) on a pinned-host FeatureBatch",
+                    cpu=cpu, parity=None)
+
+
+class StreamedOracle:
+    """The CPU oracle run layer by layer on a fixed column sample while the
+    network is generated chunk by chunk (no whole-model host copy): the C4
+    CPU baseline and its full-size parity sample. Columns are split over host
+    threads (the oracle's C call releases the GIL)."""
+
+    def __init__(self, data, cols, bias, threads):
+        self.y = np.asfortranarray(data[:, cols])
+        self.cats = np.asarray(cols, np.int64)
+        self.bias = bias
+        self.threads = threads
+        self.seconds = 0.0
+        self.counts = [len(cols)]
+
+    def __call__(self, l0, layers):
+        from concurrent.futures import ThreadPoolExecutor
+        from oracle import oracle
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            for lay in layers:
+                m = self.y.shape[1]
+                if m == 0:
+                    self.counts.append(0)
+                    continue
+                parts = np.array_split(np.arange(m), min(self.threads, m))
+                outs = list(ex.map(lambda p: oracle.layer(lay, self.bias, self.y[:, p]), parts))
+                out = np.concatenate([o for o, _ in outs], axis=1)
+                alive = np.concatenate([a for _, a in outs])
+                self.y = np.asfortranarray(out[:, alive])
+                self.cats = self.cats[alive]
+                self.counts.append(int(alive.sum()))
+        self.seconds += time.perf_counter() - t0
+
+
+def chunked_workload(args, cfg, params, batch):
+    """C4 (65536 x 1920): the network is generated, planned (C++) and uploaded
+    64 layers at a time; its 32 GB host CSR never exists at once. The CPU
+    oracle follows the same stream on a fixed 32-column sample."""
+    from paper_2007_14152_b200 import engine, ingest
+    spec = ingest.GeneratorSpec(neurons=cfg["neurons"], layers=cfg["layers"],
+                                connections_per_neuron=K_CONN, bias_value=cfg["bias"],
+                                seed=MODEL_SEED)
+    bias = ingest.synthetic_bias(spec)
+    threads = os.cpu_count() or 1
+    cols = np.sort(np.random.default_rng(123).choice(cfg["inputs"], 32, replace=False))
+    orc = StreamedOracle(np.asarray(batch.data), cols, bias, threads) \
+        if args.cpu_sample > 0 else None
+    t0 = time.time()
+    net = engine.DeviceNetwork.from_layers(ingest.iter_synthetic_layers(spec), bias,
+                                           params=params, chunk=64, on_chunk=orc)
+    log(f"generated+prepared+uploaded {net.num_layers} layers in {time.time() - t0:.1f}s "
+        f"({net.hbm_bytes / 1e9:.1f} GB of layout)"
+        + (f"; oracle sample {orc.seconds:.1f}s" if orc else ""))
+
+    def e2e(b):
+        return engine.infer_device(net, b, values=False)
+
+    def cpu(inputs):
+        if orc is None:
+            return None
+        edges = len(cols) * float(np.sum(net.nnz))
+        return {"value": edges / orc.seconds / 1e12, "unit": "TE/s", "cores": threads,
+                "kind": "port",
+                "sample": f"{len(cols)} fixed-seed columns of {cfg['inputs']} through all "
+                          f"{net.num_layers} layers, layer-streamed oracle/spdnn_oracle.c on "
+                          f"{threads} host threads ({orc.seconds:.1f} s)"}
+
+    def parity(full_cats):
+        """Full-size sampled parity: the GPU on the sample columns alone vs the
+        oracle, bit for bit; and the full run's survivors within the sample."""
+        if orc is None:
+            return None
+        from paper_2007_14152_b200.model import make_feature_batch
+        sub = make_feature_batch(cfg["neurons"], np.asfortranarray(np.asarray(batch.data)[:, cols]),
+                                 categories=cols, total_inputs=cfg["inputs"])
+        got = engine.infer_device(net, sub, values=True)
+        ok = (got.categories.tolist() == orc.cats.tolist()
+              and np.array_equal(np.asarray(got.final.data).view(np.uint32),
+                                 orc.y.view(np.uint32))
+              and np.intersect1d(full_cats, cols).tolist() == orc.cats.tolist()
+              and [o.active_before for o in got.per_layer] + [len(got.categories)]
+              == orc.counts)
+        return {"sample_columns": len(cols), "survivors_in_sample": len(orc.cats),
+                "bit_exact": bool(ok)}
+
+    return Workload(net=net, nnz=np.asarray(net.nnz, np.float64), e2e=e2e,
+                    e2e_path="engine.infer_device(values=False) on a pinned-host FeatureBatch "
+                             "(network resident, built by DeviceNetwork.from_layers)",
+                    cpu=cpu, parity=parity)
+
+
 def run_ours(args, cfg):
     import torch
-    import torch.distributed as dist
     from paper_2007_14152_b200 import _native, engine
-    from paper_2007_14152_b200.model import FeatureBatch, InferenceConfig, count_edges
 
     rank, world, local = dist_env()
+    if cfg.get("stress"):
+        return run_stress(args, cfg)
     # SPDNN_BENCH_PARALLEL=1 times the batch-parallel runner even at N=1
     # (its per-window overhead against the single-worker engine)
     if world > 1 or os.environ.get("SPDNN_BENCH_PARALLEL") == "1":
         return run_ours_multi(args, cfg)
     dev = torch.device("cuda", torch.cuda.current_device())
     t0 = time.time()
-    model, inputs = build_workload(cfg)
-    n, L = model.neurons, model.num_layers
-    # batch-parallel: contiguous category ranges (spdnn/parallel.py:142-158)
-    base, rem = divmod(inputs.active_count, world)
-    lo = rank * base + min(rank, rem)
-    hi = lo + base + (1 if rank < rem else 0)
-    shard = FeatureBatch(neurons=n, data=inputs.data[:, lo:hi],
-                         categories=inputs.categories[lo:hi], total_inputs=inputs.total_inputs)
-    m = shard.active_count
-    log(f"[rank {rank}] workload built in {time.time() - t0:.1f}s; preparing {L} layers")
-    t0 = time.time()
+    pinned, batch = pinned_inputs(cfg)
+    n, m = cfg["neurons"], cfg["inputs"]
+    log(f"inputs generated in {time.time() - t0:.1f}s")
     params = engine.PlanParams(**{k: int(v) for k, v in
                                   (kv.split("=") for kv in args.plan.split(",") if kv)})
-    prepared = engine.prepare_model(model, InferenceConfig(), "optimized", params=params)
-    net = engine.device_network(prepared, model.bias)
-    log(f"[rank {rank}] prepared+uploaded in {time.time() - t0:.1f}s "
-        f"({net.hbm_bytes / 1e6:.0f} MB of layout)")
+    W = chunked_workload(args, cfg, params, batch) if cfg.get("chunked") else \
+        resident_workload(args, cfg, params)
+    net = W.net
+    L = net.num_layers
     ws = engine.workspace(n, m, L)
-    x_dev = torch.from_numpy(np.ascontiguousarray(np.asarray(shard.data).T)).to(dev)
-    cats_dev = torch.from_numpy(np.ascontiguousarray(shard.categories)).to(dev)
+    x_dev = pinned.to(dev)
+    cats_dev = torch.from_numpy(np.ascontiguousarray(batch.categories)).to(dev)
     stream = torch.cuda.current_stream()
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
     opts = engine.run_opts(net)
 
     def step(evs=None):
@@ -377,8 +586,7 @@ def run_ours(args, cfg):
     run0 = step()
     counts_chk, cats_chk, _ = engine.collect(run0, want_values=False)
     assert run0.guard == 0, "FMA-form guard tripped on the bench workload"
-    log(f"[rank {rank}] arithmetic form: {'fma' if run0.fma else 'exact'}; "
-        f"survivors {int(counts_chk[-1])}")
+    log(f"arithmetic form: {'fma' if run0.fma else 'exact'}; survivors {int(counts_chk[-1])}")
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -387,108 +595,197 @@ def run_ours(args, cfg):
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(L + 1)] for _ in range(args.steps)]
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clocks:
-        barrier()
         torch.cuda.synchronize()
         e_start.record()
         for k in range(args.steps):
             step(evs[k])
         e_end.record()
         torch.cuda.synchronize()
-        barrier()
     ms_total = e_start.elapsed_time(e_end)
     layer_ms = np.array([[evs[k][l].elapsed_time(evs[k][l + 1]) for l in range(L)]
                          for k in range(args.steps)])
     counts = ws.counts[: L + 1].cpu().numpy().astype(np.int64)
-    if args.dump_layers and rank == 0:
+    if args.dump_layers:
         with open(args.dump_layers, "w") as f:
             json.dump({"counts": counts.tolist(), "layer_ms": layer_ms.mean(axis=0).tolist()}, f)
     ms_step = ms_total / args.steps
-    if world > 1:
-        t = torch.tensor([ms_step], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    edges_step = cfg["inputs"] * count_edges(model)  # whole job (all ranks' inputs)
+    edges_step = cfg["inputs"] * float(W.nnz.sum())  # credited: every input, every layer
     value = edges_step / (ms_step / 1e3) / 1e12
 
     # ---- roofline of the layer kernel: algorithmic bytes / CUDA-event time
-    nnz = np.array([lay.nnz for lay in model.layers], np.float64)
-    bytes_l = 8.0 * n * counts[:L] + 6.0 * nnz + 4.0 * n
+    bytes_l = 8.0 * n * counts[:L] + 6.0 * W.nnz + 4.0 * n
     active = counts[:L] > 0
     achieved = float(bytes_l[active].sum() / (layer_ms.mean(axis=0)[active].sum() / 1e3) / 1e9)
     peak, peak_src = measured_peaks()
     kernel_share = float(layer_ms.sum() / ms_total)
     traffic, traffic_src = ncu_traffic(args.config)
+    del x_dev
+    torch.cuda.empty_cache()
 
     # ---- end to end through the public API: pinned host inputs -> categories
-    pinned = torch.empty((m, n), dtype=torch.float32).pin_memory()
-    pinned.copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(shard.data).T)))
-    host_batch = FeatureBatch(neurons=n, data=pinned.numpy().T, categories=shard.categories,
-                              total_inputs=shard.total_inputs)
     e2e_steps = max(1, min(args.steps, 5))
-    res = engine.infer(model, host_batch, InferenceConfig(), prepared=prepared, values=False)
-    barrier()
+    res = W.e2e(batch)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        res = engine.infer(model, host_batch, InferenceConfig(), prepared=prepared, values=False)
+        res = W.e2e(batch)
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
     assert np.array_equal(res.categories, cats_chk.cpu().numpy()), "e2e categories differ"
     h2d = m * n * 4 + m * 8
     d2h = len(res.categories) * 8 + (L + 1) * 4
+    parity = W.parity(res.categories) if W.parity else None
+    if parity is not None:
+        log(f"full-size sampled parity: {parity}")
+        assert parity["bit_exact"], "GPU differs from the oracle on the sampled columns"
 
-    line = None
+    cpu = W.cpu(batch) if args.cpu_sample > 0 else None
+    line = {
+        "metric": "TeraEdges/s", "value": value, "unit": "TE/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
+                   "input_density": cfg["density"], "connections": K_CONN,
+                   "survivors": int(counts[L]), "sum_active": int(counts[:L].sum()),
+                   "l2": "inputs larger than L2 (Y = %.0f MB per buffer vs 126 MB)"
+                         % (n * ws.ld * 4 / 1e6),
+                   "parallelism": "single",
+                   "arithmetic": "fma form (weights 2^-4, guard clean)" if opts.fma_form
+                                 else "exact form",
+                   "plan": dataclasses.asdict(params),
+                   "layout_hbm_gb": round(net.hbm_bytes / 1e9, 2)},
+        "e2e": {"value": edges_step / e2e_s / 1e12, "unit": "TE/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_s * 1e3, "path": W.e2e_path},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": (f"profiles/{traffic_src}: dram read+write of one "
+                                        "steady-state launch (ncu --set full)")
+                                       if traffic else None,
+                     "peak_source": peak_src,
+                     "kernel": "layer_kernel (csrc/layer.cu)",
+                     "bytes_per_launch": "8*N*M_l + 6*nnz_l + 4*N",
+                     "kernel_share_of_step": kernel_share,
+                     "active_edge_rate_T": float(counts[:L].sum() * K_CONN * n /
+                                                 (ms_step / 1e3) / 1e12)},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+        "gpu_launches": args.steps * (L + 1),
+    }
+    if parity is not None:
+        line["parity"] = parity
+    print(json.dumps(line), flush=True)
+    return line
+
+
+def stress_inputs(cfg):
+    """C5: 8 contiguous shards of 7500 inputs, shard s drawn
+    at density |b| + 0.04 - 0.01 s with seed 100 + s -- the same recipe as
+    tests/golden/make_stress.py, here on config 3's network."""
+    from paper_2007_14152_b200 import ingest
+    from paper_2007_14152_b200.model import make_feature_batch
+    n, w, per = cfg["neurons"], cfg["workers"], cfg["inputs"] // cfg["workers"]
+    parts = [np.asarray(ingest.generate_synthetic_inputs(
+        n, per, abs(cfg["bias"]) + 0.04 - 0.01 * s, seed=100 + s).data) for s in range(w)]
+    return make_feature_batch(n, np.concatenate(parts, axis=1))
+
+
+def balance_summary(bal, shard_sizes):
+    """Per-layer work model of the 8-GPU run: layer l+1's time on worker w is
+    proportional to the features it holds after layer l's (re)balancing, and
+    every layer ends at the slowest worker (the count exchange is a barrier).
+    time-weighted max/mean = sum_l max_w / sum_l mean_w (1.0 = perfect)."""
+    inputs = [list(shard_sizes)] + [list(e.after_counts) for e in bal.entries[:-1]]
+    mx = sum(max(c) for c in inputs)
+    mean = sum(sum(c) / len(c) for c in inputs)
+    ratios = [e.imbalance_before for e in bal.entries if np.isfinite(e.imbalance_before)]
+    return {"time_weighted_max_over_mean": mx / mean if mean else 1.0,
+            "max_imbalance_before": max(ratios) if ratios else 1.0,
+            "max_imbalance_after": max((e.imbalance_after for e in bal.entries
+                                        if np.isfinite(e.imbalance_after)), default=1.0),
+            "rebalances": int(sum(e.rebalanced for e in bal.entries)),
+            "rows_moved": int(bal.total_moved)}
+
+
+def run_stress(args, cfg):
+    """C5: skewed shards, rebalancing on (threshold 1.25) vs off (inf).
+    N = 1: the 8 workers share this GPU (parallel.run_batch_parallel's
+    in-process transport), so the device time is the SUM over workers and the
+    8-GPU effect is reported through the count-based work model
+    (balance_summary). N = 8 under torchrun: one worker per GPU over NCCL,
+    timed as the max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2007_14152_b200 import engine, ingest, parallel
+    from paper_2007_14152_b200.model import InferenceConfig, count_edges
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+        dist.init_process_group(os.environ.get("SPDNN_DIST_BACKEND", "nccl"),
+                                init_method="env://")
+        if world != cfg["workers"]:
+            log(f"C5 is defined for {cfg['workers']} workers; running with {world}")
+    workers = world if world > 1 else cfg["workers"]
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=cfg["neurons"], layers=cfg["layers"], connections_per_neuron=K_CONN,
+        bias_value=cfg["bias"], seed=MODEL_SEED))
+    inputs = stress_inputs(dict(cfg, workers=workers))
+    prepared = engine.prepare_model(model, InferenceConfig(), "optimized")
+    edges = inputs.total_inputs * count_edges(model)
+    bounds = parallel.shard_bounds(inputs.active_count, workers)
+    sizes = [hi - lo for lo, hi in bounds]
+    out = {}
+    for tag, thr in (("on", 1.25), ("off", float("inf"))):
+        conf = InferenceConfig(workers=workers, rebalance_threshold=thr)
+        for _ in range(max(1, args.warmup)):
+            res, comm, bal = parallel.run_batch_parallel(model, inputs, conf,
+                                                         prepared=prepared, values=False)
+        times = []
+        with ClockSampler(torch.cuda.current_device()) as clocks:
+            for _ in range(args.steps):
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                res, comm, bal = parallel.run_batch_parallel(model, inputs, conf,
+                                                             prepared=prepared, values=False)
+                e1.record()
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1)
+                if world > 1:
+                    tt = torch.tensor([t], device="cuda")
+                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                    t = float(tt.item())
+                times.append(t)
+        ms = float(np.median(times))
+        out[tag] = dict(balance_summary(bal, sizes), ms_per_step=ms,
+                        value=edges / (ms / 1e3) / 1e12, survivors=len(res.categories),
+                        clocks=clocks.summary(), categories=res.categories)
+    same = np.array_equal(out["on"].pop("categories"), out["off"].pop("categories"))
     if rank == 0:
-        cpu = None
-        if world == 1 and args.cpu_sample > 0:
-            threads = os.cpu_count() or 1
-            r = cpu_baseline(model, inputs, args.cpu_sample, threads,
-                             target_s=args.cpu_seconds)
-            cpu = {"value": r["value"], "unit": "TE/s", "cores": threads, "kind": "port",
-                   "sample": f"first {r['sample_cols']} of {cfg['inputs']} inputs, all "
-                             f"{L} layers, oracle/spdnn_oracle.c on {threads} host threads "
-                             f"({r['seconds']:.1f} s)"}
+        on, off = out["on"], out["off"]
         line = {
-            "metric": "TeraEdges/s", "value": value, "unit": "TE/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "metric": "TeraEdges/s", "value": on["value"], "unit": "TE/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": on["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
-                       "input_density": cfg["density"], "connections": K_CONN,
-                       "survivors": int(counts[L]), "sum_active": int(counts[:L].sum()),
-                       "l2": "inputs larger than L2 (Y = %.0f MB per buffer vs 126 MB)"
-                             % (n * ws.ld * 4 / 1e6),
-                       "parallelism": f"batch-parallel x{world}" if world > 1 else "single",
-                       "arithmetic": "fma form (weights 2^-4, guard clean)" if opts.fma_form
-                                     else "exact form",
-                       "plan": dataclasses.asdict(params)},
-            "e2e": {"value": edges_step / e2e_s / 1e12, "unit": "TE/s",
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_s * 1e3,
-                    "path": "engine.infer(values=False) on a pinned-host FeatureBatch"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "traffic_source": (f"profiles/{traffic_src}: dram read+write of one "
-                                            "steady-state launch (ncu --set full)")
-                                           if traffic else None,
-                         "peak_source": peak_src,
-                         "kernel": "layer_kernel (csrc/layer.cu)",
-                         "bytes_per_launch": "8*N*M_l + 6*nnz_l + 4*N",
-                         "kernel_share_of_step": kernel_share,
-                         "active_edge_rate_T": float(counts[:L].sum() * K_CONN * n /
-                                                     (ms_step / 1e3) / 1e12)},
-            "cpu_baseline": cpu,
-            "clocks": clocks.summary(),
-            "gpu_launches": args.steps * (L + 1),
+            "config": {"workload": cfg["name"], "inputs": inputs.total_inputs,
+                       "workers": workers,
+                       "shards": f"{workers} x {sizes[0]}, density |b|+0.04-0.01*s, seed 100+s",
+                       "transport": "NCCL, one worker per GPU" if world > 1 else
+                                    "in-process: all workers on this GPU (time = sum)",
+                       "categories_identical_on_off": bool(same)},
+            "rebalancing_on": on, "rebalancing_off": off,
+            "modelled_8gpu_speedup_from_rebalancing":
+                off["time_weighted_max_over_mean"] / on["time_weighted_max_over_mean"],
+            "clocks": on["clocks"], "gpu_launches": None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-    return line
 
 
 def main():

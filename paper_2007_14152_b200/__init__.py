@@ -9,9 +9,12 @@ reference's Python API (``spdnn/__init__.py:9-63``) name for name.
 from .model import (FeatureBatch, InferenceConfig, LayerCSR, ModelError, NetworkModel,
                     count_edges, make_feature_batch, make_layer_csr, relu_clamped,
                     validate_model)
-from .ingest import GeneratorSpec, generate_synthetic_inputs, generate_synthetic_network
+from .ingest import (GeneratorSpec, IngestError, generate_synthetic_inputs,
+                     generate_synthetic_network, iter_synthetic_layers, load_features_tsv,
+                     load_layer_tsv, load_truth_categories, read_binary, write_binary)
 from .engine import (InferenceResult, LayerOutcome, LayerPlan, PaddingStats, PlanParams,
-                     PreparedLayer, baseline_layer, compact_active, infer, optimized_layer,
+                     PreparedLayer, WeightStreamer, baseline_layer, compact_active, infer,
+                     infer_device, optimized_layer,
                      prepare_model, run_layer_step)
 from .parallel import (BalanceEntry, BalanceReport, CommMatrix, CountMsg, GatherMsg, Partition,
                        RowsMsg, apply_transfers, balance_step, gather_categories,

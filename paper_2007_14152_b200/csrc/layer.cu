@@ -326,6 +326,18 @@ __device__ __forceinline__ float min_nan(float a, float b) {
   return r;
 }
 
+// The clamp of a value that is not NaN and not -0 (the FMA form's inputs are
+// screened so sums stay finite, and round-to-nearest never yields -0 here):
+// on the float bit pattern read as int32, order is preserved among
+// non-negatives and every negative float is a negative int, so
+// min(bits, bits(32)) followed by relu is min(max(v, 0), 32) -- one
+// instruction (min.relu.s32) instead of two FMNMX.
+__device__ __forceinline__ float clamp_finite(float v) {
+  int r;
+  asm("min.relu.s32 %0, %1, %2;" : "=r"(r) : "r"(__float_as_int(v)), "r"(0x42000000));
+  return __int_as_float(r);
+}
+
 // Bias, clamp, store for one finished group; returns the lane's activity bits.
 // All rows are finished into the accumulator registers first and stored
 // after, so no store's source registers are overwritten while it is queued.
@@ -351,8 +363,13 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
 #pragma unroll
     for (int h = 0; h < H; h++) {
       float2 v = __fadd2_rn(*reinterpret_cast<float2 *>(&acc[H * k + h]), b2);
-      v.x = min_nan(max_nan(v.x, 0.0f), 32.0f);
-      v.y = min_nan(max_nan(v.y, 0.0f), 32.0f);
+      if (FMA) {
+        v.x = clamp_finite(v.x);
+        v.y = clamp_finite(v.y);
+      } else {
+        v.x = min_nan(max_nan(v.x, 0.0f), 32.0f);
+        v.y = min_nan(max_nan(v.y, 0.0f), 32.0f);
+      }
       *reinterpret_cast<float2 *>(&acc[H * k + h]) = v;
     }
   }
@@ -460,7 +477,7 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ int s_done[kMaxBufs];
-  __shared__ int s_pitem;
+  __shared__ int s_pitem[2];
 
   using G = Geo<FPL>;
   constexpr int RW = Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
@@ -498,10 +515,47 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
     const int pw = warp - C;
     const int ptid = pw * 32 + lane;
     auto pbar = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(P * 32) : "memory"); };
+    // Item metadata is fetched one item ahead: the next item's index (atomic),
+    // block descriptor, feature columns and first staged-row quad are loaded
+    // while this item's slot is awaited and its copies are issued, so none of
+    // those global round trips sits between a slot turning free and its fill.
+    struct ItemMeta {
+      int item, t, b, v, c4x, c4y, c4z, c4w;
+      int src[FPL];
+    };
+    auto fetch = [&](int item, ItemMeta &im) {
+      im.item = item;
+      if (item >= items) return;
+      im.t = item / nb;
+      im.b = item - im.t * nb;
+      im.v = lane < 8 ? __ldg(A.L.blocks + (int64_t)im.b * 8 + lane) : 0;
+      const int valid = min(T, M - im.t * T);
+#pragma unroll
+      for (int q = 0; q < FPL; q++) {
+        const int f = 32 * q + lane;
+        im.src[q] = f < valid ? __ldg(A.a_in + im.t * T + f) : -1;
+      }
+      // this thread's first staged-row quad (contiguous path)
+      const int meta_off = __shfl_sync(0xffffffffu, im.v, 4);
+      const int fp_cnt = __shfl_sync(0xffffffffu, im.v, 5);
+      const int32_t *fp = A.L.meta + meta_off;
+      const int qd = ptid;
+      if (4 * qd + 3 < fp_cnt) {
+        const int4 c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
+        im.c4x = c4.x; im.c4y = c4.y; im.c4z = c4.z; im.c4w = c4.w;
+      } else if (4 * qd < fp_cnt) {
+        im.c4x = __ldg(fp + 4 * qd);
+        im.c4y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : im.c4x;
+        im.c4z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : im.c4x;
+        im.c4w = im.c4x;
+      }
+    };
+    ItemMeta cur;
+    if (ptid == 0) s_pitem[0] = atomicAdd(A.work, 1);
+    pbar();
+    fetch(s_pitem[0], cur);
     for (int k = 0;; k++) {
-      if (ptid == 0) s_pitem = atomicAdd(A.work, 1);
-      pbar();
-      const int item = s_pitem;
+      const int item = cur.item;
       if (item >= items) {
         if (pw == 0) {
           // end markers in the next nbuf entries; a consumer warp waits at most
@@ -520,9 +574,9 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
         }
         break;
       }
-      const int t = item / nb;
-      const int b = item - t * nb;
-      const int v = lane < 8 ? __ldg(A.L.blocks + (int64_t)b * 8 + lane) : 0;
+      int nxt = 0;
+      if (ptid == 0) nxt = atomicAdd(A.work, 1);  // consumed after this item's copies
+      const int t = cur.t, b = cur.b, v = cur.v;
       const int ng = __shfl_sync(0xffffffffu, v, 1);
       const int nst = __shfl_sync(0xffffffffu, v, 2);
       const int meta_off = __shfl_sync(0xffffffffu, v, 4);
@@ -531,19 +585,11 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
       const int rec_cnt = __shfl_sync(0xffffffffu, v, 7);
       // feature columns 32q + lane (q < FPL) of tile t: gathers then write 32
       // consecutive smem words per instruction (bank-conflict free)
-      const int valid = min(T, M - t * T);
-      int src[FPL];
-      bool ok[FPL];
-#pragma unroll
-      for (int q = 0; q < FPL; q++) {
-        const int f = 32 * q + lane;
-        ok[q] = f < valid;
-        src[q] = ok[q] ? __ldg(A.a_in + t * T + f) : 0;
-      }
-      const int p0 = __shfl_sync(0xffffffffu, src[0], 0);
+      const int p0 = __shfl_sync(0xffffffffu, cur.src[0], 0);
       bool mine_contig = true;
 #pragma unroll
-      for (int q = 0; q < FPL; q++) mine_contig &= !ok[q] || src[q] == p0 + 32 * q + lane;
+      for (int q = 0; q < FPL; q++)
+        mine_contig &= cur.src[q] < 0 || cur.src[q] == p0 + 32 * q + lane;
       const bool contig = __all_sync(0xffffffffu, mine_contig) && (p0 & 3) == 0;
 
       const int slot = k % nbuf;
@@ -567,7 +613,10 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
       if (ptid == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
       const int32_t *fp = A.L.meta + meta_off;
       if (contig) {
-        for (int qd = ptid; qd < quads; qd += P * 32) {
+        if (ptid < quads)
+          tma_gather4(sy + (uint32_t)ptid * 4u * G::kRow, &A.tmap_in, p0, cur.c4x, cur.c4y,
+                      cur.c4z, cur.c4w, full);
+        for (int qd = ptid + P * 32; qd < quads; qd += P * 32) {  // footprints > 512 rows
           int4 c4;
           if (4 * qd + 3 < fp_cnt) {
             c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
@@ -590,12 +639,16 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
             const float *row = A.y_in + c * A.ld;
             const uint32_t dst = sy + (uint32_t)(s0 + i) * G::kRow + 4 * lane;
 #pragma unroll
-            for (int q = 0; q < FPL; q++) cp_async4(dst + 128 * q, row + src[q], ok[q]);
+            for (int q = 0; q < FPL; q++)
+              cp_async4(dst + 128 * q, row + max(cur.src[q], 0), cur.src[q] >= 0);
           }
         }
         mbar_cp_async_arrive_inc(full);
       }
-      pbar();  // every producer's copies issued and counted
+      // s_pitem is double-buffered: entry (k+1)&1 was last read before this
+      // iteration's first barrier
+      if (ptid == 0) s_pitem[(k + 1) & 1] = nxt;
+      pbar();  // every producer's copies issued and counted; next item index visible
       if (ptid == 0) {
         Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
         h->item = item;
@@ -608,6 +661,7 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
         h->fp_cnt = fp_cnt;
         mbar_arrive(full);
       }
+      fetch(s_pitem[(k + 1) & 1], cur);
     }
     return;
   }

@@ -251,32 +251,87 @@ def _fill_bias_slots(plan: "LayerPlan", meta: np.ndarray, bias: np.ndarray) -> n
     return meta
 
 
+_KINDS = ("blocks", "stages", "meta", "records")
+
+
 class DeviceNetwork:
     """All layer plans of a network resident in HBM, plus the bias vector.
 
-    Arrays of all layers are concatenated per kind (one allocation each);
-    ``layer_devs`` holds one ``spdnn_layer_dev`` per layer pointing into them.
+    Plans are uploaded in chunks of layers; within a chunk the arrays of all
+    its layers are concatenated per kind (one allocation each). ``layer_devs``
+    holds one ``spdnn_layer_dev`` per layer pointing into them. Built either
+    from a prepared model (``DeviceNetwork(prepared, bias)``) or layer chunk by
+    layer chunk from a CSR iterator (``DeviceNetwork.from_layers``), which never
+    holds more than one chunk of host CSR/plans -- the 65536 x 1920 network's
+    CSR alone is 32 GB of host memory, its layout 25 GB of HBM.
     """
 
     def __init__(self, prepared: Sequence[PreparedLayer], bias: np.ndarray, device=None):
+        self._start(bias, device)
+        self.modes = {p.mode for p in prepared}
+        self.nnz = [p.csr.nnz if p.csr is not None else 0 for p in prepared]
+        self._append([p.plan for p in prepared])
+        self._finish()
+
+    @classmethod
+    def from_layers(cls, layers, bias: np.ndarray, params: "PlanParams | None" = None,
+                    chunk: int = 64, threads: int = 0, on_chunk=None, device=None
+                    ) -> "DeviceNetwork":
+        """Plan (C++, host threads) and upload `layers` (any iterable of
+        LayerCSR) `chunk` layers at a time. ``on_chunk(first_layer_index,
+        csr_list)`` sees each chunk's CSR before it is dropped (e.g. a
+        layer-by-layer CPU check)."""
+        self = cls.__new__(cls)
+        self._start(bias, device)
+        params = params or OPTIMIZED_PARAMS
+        self.modes = {"baseline" if params == BASELINE_PARAMS else "optimized"}
+        self.nnz = []
+        buf = []
+
+        def flush():
+            plans = build_plans(buf, params, threads)
+            if on_chunk is not None:
+                on_chunk(self.num_layers, list(buf))
+            self.nnz += [lay.nnz for lay in buf]
+            self._append(plans)
+            buf.clear()
+
+        for lay in layers:
+            if lay.neurons != self.neurons:
+                raise ModelError("layer width does not match the bias vector")
+            buf.append(lay)
+            if len(buf) == chunk:
+                flush()
+        if buf:
+            flush()
+        self._finish()
+        return self
+
+    def _start(self, bias, device):
         torch = _torch()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
-        self.num_layers = len(prepared)
         self.neurons = int(bias.shape[0])
-        self.modes = {p.mode for p in prepared}
-        plans = [p.plan for p in prepared]
-        kinds = ("blocks", "stages", "meta", "records")
-        self.buffers = {}
-        offsets = {k: [] for k in kinds}
-        bias32 = np.ascontiguousarray(bias, np.float32)
-        for k in kinds:
+        self._bias32 = np.ascontiguousarray(bias, np.float32)
+        self.bias = torch.from_numpy(self._bias32.copy()).to(self.device)
+        self.num_layers = 0
+        self.chunks = []        # per chunk: {kind: device tensor}
+        self._ptrs = []         # per layer: {kind: device address}
+        self._plans_meta = []   # per layer: the LayerPlan scalars (arrays dropped)
+        self.total_slots, self.num_fp = [], []
+        self.pow2, self._emin, self._emax = True, None, None
+        self.hbm_bytes = int(self.bias.numel() * 4)
+
+    def _append(self, plans) -> None:
+        torch = _torch()
+        bufs, offsets = {}, {k: [] for k in _KINDS}
+        for k in _KINDS:
             parts = []
             off = 0
             for pl in plans:
                 a = getattr(pl, k)
                 if k == "meta":
-                    a = _fill_bias_slots(pl, a, bias32)
+                    a = _fill_bias_slots(pl, a, self._bias32)
                 pad = (-a.shape[0] * a.itemsize) % 32  # every layer's slice 32-byte aligned
                 parts.append(a)
                 if pad:
@@ -288,15 +343,26 @@ class DeviceNetwork:
                 cat = cat.view(np.int32)
             if cat.size == 0:
                 cat = np.zeros(1, dtype=cat.dtype)
-            self.buffers[k] = torch.from_numpy(np.ascontiguousarray(cat)).to(self.device)
-        self.bias = torch.from_numpy(np.ascontiguousarray(bias, np.float32)).to(self.device)
-        self.layer_devs = (_native.LayerDev * max(1, self.num_layers))()
-        self.max_fp = 0
+            bufs[k] = torch.from_numpy(np.ascontiguousarray(cat)).to(self.device)
+            self.hbm_bytes += int(bufs[k].numel() * bufs[k].element_size())
+        self.chunks.append(bufs)
         for l, pl in enumerate(plans):
+            self._ptrs.append({k: bufs[k].data_ptr() + offsets[k][l] * bufs[k].element_size()
+                               for k in _KINDS})
+            self._plans_meta.append(pl)
+            self.total_slots.append(pl.total_slots)
+            self.num_fp.append(pl.num_fp)
+            self.pow2 = self.pow2 and pl.pow2
+            self._emin = pl.wexp_min if self._emin is None else min(self._emin, pl.wexp_min)
+            self._emax = pl.wexp_max if self._emax is None else max(self._emax, pl.wexp_max)
+        self.num_layers += len(plans)
+
+    def _finish(self) -> None:
+        self.layer_devs = (_native.LayerDev * max(1, self.num_layers))()
+        for l, pl in enumerate(self._plans_meta):
             d = self.layer_devs[l]
-            for k in kinds:
-                buf = self.buffers[k]
-                setattr(d, k, buf.data_ptr() + offsets[k][l] * buf.element_size())
+            for k in _KINDS:
+                setattr(d, k, self._ptrs[l][k])
             d.num_blocks = pl.num_blocks
             d.neurons = pl.neurons
             d.rows_per_group = pl.rows_per_group
@@ -304,21 +370,20 @@ class DeviceNetwork:
             d.max_fp_per_stage = pl.max_fp_per_stage
             d.max_records_per_stage = pl.max_records_per_stage
             d.max_meta_per_block = pl.max_meta_per_block
-            # one launch serves all layers' items with the same unit count
             d.max_groups_per_block = pl.max_groups_per_block
+        self._plans_meta = [None] * self.num_layers  # host arrays no longer needed
         # FMA form (one FFMA2 per (row, column)) is exact when every weight is
         # +-2^e and no input falls below `tiny` (products stay normal) or above
         # `huge` (no overflow); the kernels flag violations and infer() reruns
         # in the exact form.
-        self.pow2 = bool(plans) and all(pl.pow2 for pl in plans)
-        emin = min((pl.wexp_min for pl in plans), default=0)
-        emax = max((pl.wexp_max for pl in plans), default=0)
+        self.pow2 = self.num_layers > 0 and self.pow2
+        emin = self._emin if self._emin is not None else 0
+        emax = self._emax if self._emax is not None else 0
         self.tiny = float(np.ldexp(np.float32(1.0), -126 - emin)) if -126 - emin > -149 else 0.0
         self.tiny = min(self.tiny, 1.0)
-        self.huge = float(np.ldexp(1.0, min(127, 126 - emax))) if emax < 126 else 0.0
-        self.total_slots = [pl.total_slots for pl in plans]
-        self.num_fp = [pl.num_fp for pl in plans]
-        self.hbm_bytes = sum(int(b.numel() * b.element_size()) for b in self.buffers.values())
+        # |x| <= huge keeps every product <= 2^95 and every sum of up to 2^31
+        # of them finite (the FMA form's integer clamp assumes no NaN/inf)
+        self.huge = float(np.ldexp(1.0, min(127, 95 - emax))) if emax < 95 else 0.0
 
 
 class Workspace:
@@ -514,24 +579,50 @@ def infer(model: NetworkModel, inputs: FeatureBatch, config: InferenceConfig,
     with CUDA events. ``values=False`` (extension) skips copying the final
     feature values back: ``final`` is then None and only the sorted
     categories and per-layer counts come back -- the Graph Challenge output.
+    With ``config.streaming`` the layouts are built by a WeightStreamer while
+    the GPU runs the previous layers (engine.py:173-232, 250-282).
     """
     _check_inputs(model, inputs, mode)
-    if config.streaming and prepared is not None:
-        raise ModelError("prepared structures cannot be combined with streaming")
+    if config.streaming:
+        if prepared is not None:
+            raise ModelError("prepared structures cannot be combined with streaming")
+        return _infer_streaming(model, inputs, config, mode, values)
     if prepared is None:
         prepared = prepare_model(model, config, mode)
     _check_prepared(prepared, model, mode)
-    torch = _torch()
     n, m = model.neurons, inputs.active_count
     if model.num_layers == 0 or m == 0:
-        per = [LayerOutcome(0, 0, 0, 0) for _ in range(model.num_layers)]
-        if m and model.num_layers == 0:
-            per = []
-        return InferenceResult(final=inputs, categories=inputs.categories.copy(),
-                               per_layer=per, elapsed_seconds=0.0,
-                               edges_processed=inputs.total_inputs * count_edges(model))
+        return _trivial_result(model.num_layers, inputs, count_edges(model))
     net = device_network(prepared, model.bias)
-    ws = workspace(n, m, model.num_layers)
+    return infer_device(net, inputs, values=values, edges_per_input=count_edges(model),
+                        unpadded=lambda: DeviceNetwork(_unpadded(prepared, model), model.bias))
+
+
+def _trivial_result(num_layers: int, inputs: FeatureBatch, edges: int) -> InferenceResult:
+    m = inputs.active_count
+    per = [LayerOutcome(0, 0, 0, 0) for _ in range(num_layers)]
+    if m and num_layers == 0:
+        per = []
+    return InferenceResult(final=inputs, categories=inputs.categories.copy(), per_layer=per,
+                           elapsed_seconds=0.0, edges_processed=inputs.total_inputs * edges)
+
+
+def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
+                 edges_per_input: int | None = None, unpadded=None) -> InferenceResult:
+    """``infer`` on a network already resident in HBM (extension): e.g. one
+    built layer chunk by layer chunk with ``DeviceNetwork.from_layers`` for a
+    model whose host CSR would not fit. ``unpadded()`` returns the same
+    network with one row per group; it is only called for non-finite inputs
+    (see DESIGN.md section 3)."""
+    torch = _torch()
+    n, m = net.neurons, inputs.active_count
+    if inputs.neurons != n:
+        raise ModelError("inputs do not match model width")
+    edges = inputs.total_inputs * (edges_per_input if edges_per_input is not None
+                                   else sum(getattr(net, "nnz", [])))
+    if net.num_layers == 0 or m == 0:
+        return _trivial_result(net.num_layers, inputs, edges // max(inputs.total_inputs, 1))
+    ws = workspace(n, m, net.num_layers)
     x = torch.from_numpy(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
     cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
     fma = None
@@ -548,11 +639,16 @@ def infer(model: NetworkModel, inputs: FeatureBatch, config: InferenceConfig,
         elapsed += time.perf_counter() - t0
         device += ev0.elapsed_time(ev1) / 1e3
         counts, sorted_cats, vals = collect(run, want_values=values)
-        if run.needs_unpadded_rerun:
+        if run.needs_unpadded_rerun and unpadded is not None:
             # NaN/inf inputs: zero-weight union slots would spread them to rows
             # that never read them; one row per group has no such slots.
-            net = DeviceNetwork(_unpadded(prepared, model), model.bias)
+            net = unpadded()
+            unpadded = None
             fma = False
+        elif run.needs_unpadded_rerun:
+            if all(d.rows_per_group == 1 for d in net.layer_devs[: net.num_layers]):
+                break
+            raise ModelError("non-finite inputs need the unpadded plans")
         elif run.needs_exact_rerun:
             fma = False
         else:
@@ -564,8 +660,177 @@ def infer(model: NetworkModel, inputs: FeatureBatch, config: InferenceConfig,
                              total_inputs=inputs.total_inputs)
     return InferenceResult(final=final, categories=cats_np.copy(),
                            per_layer=_outcomes(counts, net), elapsed_seconds=elapsed,
-                           edges_processed=inputs.total_inputs * count_edges(model),
-                           device_seconds=device)
+                           edges_processed=edges, device_seconds=device)
+
+
+class WeightStreamer:
+    """Double-buffered layer layouts (the reference's WeightStreamer,
+    engine.py:173-232): a background thread builds layer l+1's plan (C++,
+    the GIL released) while the GPU runs layer l; at most two layers'
+    prepared structures exist at once. Same consumer API: ``next_layer``,
+    ``release``, ``stop``, ``join``, ``peak_resident``, ``materialized_count``.
+    """
+
+    def __init__(self, model: NetworkModel, config: InferenceConfig, mode: Mode = "optimized"):
+        import queue
+        self._slots = threading.Semaphore(2)
+        self._ready = queue.Queue()
+        self._stopped = threading.Event()
+        self._gauge_lock = threading.Lock()
+        self._resident = 0
+        self.peak_resident = 0
+        self.materialized_count = 0
+        self._thread = threading.Thread(target=self._produce, args=(model, config, mode),
+                                        daemon=True)
+        self._thread.start()
+
+    def _produce(self, model, config, mode) -> None:
+        try:
+            for layer in model.layers:
+                while not self._slots.acquire(timeout=0.05):
+                    if self._stopped.is_set():
+                        return
+                if self._stopped.is_set():
+                    return
+                prep = prepare_layer(layer, config, mode)
+                with self._gauge_lock:
+                    self._resident += 1
+                    self.materialized_count += 1
+                    self.peak_resident = max(self.peak_resident, self._resident)
+                self._ready.put(prep)
+            self._ready.put(None)
+        except BaseException as exc:  # propagate into the consumer
+            self._ready.put(exc)
+
+    def next_layer(self) -> PreparedLayer:
+        item = self._ready.get()
+        if isinstance(item, BaseException):
+            raise item
+        if item is None:
+            raise ModelError("weight streamer exhausted")
+        return item
+
+    def release(self) -> None:
+        with self._gauge_lock:
+            self._resident -= 1
+        self._slots.release()
+
+    def stop(self) -> None:
+        self._stopped.set()
+        self._thread.join()
+
+    def join(self) -> None:
+        self._thread.join()
+
+
+def _infer_streaming(model: NetworkModel, inputs: FeatureBatch, config: InferenceConfig,
+                     mode: Mode, values: bool) -> InferenceResult:
+    """Layer loop fed by a WeightStreamer. Each layer's plan is uploaded and
+    its kernel enqueued as soon as the producer has it; the host never waits
+    for the GPU inside the loop except to notice that every feature died
+    (a non-blocking read of an earlier layer's count), which stops the
+    streamer as the reference does (engine.py:265-270)."""
+    torch = _torch()
+    n, m, L = model.neurons, inputs.active_count, model.num_layers
+    edges = count_edges(model)
+    if L == 0 or m == 0:
+        return _trivial_result(L, inputs, edges)
+    bias = np.asarray(model.bias, np.float32)
+    ws = workspace(n, m, L)
+    x = torch.from_numpy(np.asarray(inputs.data).T)
+    cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
+    stage_inputs(ws, x, cats, None)  # tiny = 0: screens only non-finite inputs
+    ws.counts.zero_()
+    ws.counts[0] = m
+    ws.work.zero_()
+    host_counts = torch.zeros(L + 1, dtype=torch.int32).pin_memory()
+    stream = _stream_ptr(torch)
+    main, up = torch.cuda.current_stream(), torch.cuda.Stream()
+    lib = _native.lib()
+    nets, checks, slots, fps = [], [], [], []
+    opts = None
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    streamer = WeightStreamer(model, config, mode)  # inside the clock, as engine.py:258-261
+    ran = 0
+    try:
+        for l in range(L):
+            # stop once an earlier layer's count has landed as zero
+            while checks and checks[0][1].query():
+                lc, _ = checks.pop(0)
+                if int(host_counts[lc]) == 0:
+                    raise StopIteration
+            prep = streamer.next_layer()
+            try:
+                # upload on a side stream: a pageable H2D copy on the compute
+                # stream would make the host wait for the running layer
+                with torch.cuda.stream(up):
+                    net = DeviceNetwork([prep], bias)
+            finally:
+                streamer.release()
+            ready = torch.cuda.Event()
+            ready.record(up)
+            main.wait_event(ready)
+            for t in list(net.chunks[0].values()) + [net.bias]:
+                t.record_stream(main)
+            if opts is None:
+                # the exact form throughout: the FMA form's guard would need a
+                # rerun of already-streamed layers
+                opts = run_opts(net, fma=False)
+            i, o = l & 1, (l & 1) ^ 1
+            cnt = ws.counts.data_ptr()
+            _native.check(lib.spdnn_layer_forward(
+                ctypes.byref(net.layer_devs[0]), _dptr(net.bias), _dptr(ws.y[i]),
+                _dptr(ws.y[o]), ws.ld, _dptr(ws.a[i]), _dptr(ws.cat[i]),
+                ctypes.c_void_p(cnt + 4 * l), _dptr(ws.a[o]), _dptr(ws.cat[o]),
+                ctypes.c_void_p(cnt + 4 * (l + 1)), ctypes.byref(ws.scratch),
+                ctypes.c_void_p(ws.work.data_ptr() + 4 * l), ctypes.byref(opts), stream),
+                "spdnn_layer_forward")
+            slots.append(net.total_slots[0])
+            fps.append(net.num_fp[0])
+            nets.append(net)
+            host_counts[l + 1: l + 2].copy_(ws.counts[l + 1: l + 2], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            checks.append((l + 1, ev))
+            ran = l + 1
+            if len(nets) > 2:
+                # stream-ordered allocator: the freed plan is reused only by
+                # work enqueued after this layer's kernel on the same stream
+                nets.pop(0)
+    except StopIteration:
+        pass
+    finally:
+        streamer.stop()
+    ev1.record()
+    torch.cuda.synchronize()
+    elapsed = time.perf_counter() - t0
+    run = DeviceRun(ws, ran, m)
+    run.out_index = ran % 2
+    counts, sorted_cats, vals = collect(run, want_values=values)
+    if run.needs_unpadded_rerun:
+        # non-finite inputs: redo without streaming on one-row-per-group plans
+        return infer(model, inputs, replace(config, streaming=False), mode, values=values)
+    per = []
+    for l in range(L):
+        before = int(counts[l]) if l < ran else 0
+        after = int(counts[l + 1]) if l < ran else 0
+        if before == 0:
+            per.append(LayerOutcome(0, 0, 0, 0))
+            continue
+        per.append(LayerOutcome(before, after,
+                                weight_element_reads=slots[l] * -(-before // TILE),
+                                feature_element_reads=fps[l] * before))
+    cats_np = sorted_cats.cpu().numpy().astype(np.int64)
+    final = None
+    if values:
+        final = FeatureBatch(neurons=n, data=vals.cpu().numpy().T, categories=cats_np,
+                             total_inputs=inputs.total_inputs)
+    return InferenceResult(final=final, categories=cats_np.copy(), per_layer=per,
+                           elapsed_seconds=elapsed, edges_processed=inputs.total_inputs * edges,
+                           device_seconds=ev0.elapsed_time(ev1) / 1e3)
 
 
 def _unpadded(prepared: Sequence[PreparedLayer], model: NetworkModel) -> list:

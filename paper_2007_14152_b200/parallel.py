@@ -657,7 +657,6 @@ def run_batch_parallel(model: NetworkModel, inputs: FeatureBatch, config: Infere
     """Inference across ``config.workers`` shards with per-layer balancing
     (parallel.py:379-454). Returns (InferenceResult, CommMatrix, BalanceReport);
     under torch.distributed every rank returns the same merged result."""
-    import torch
     from . import engine
 
     if inputs.neurons != model.neurons:
@@ -667,16 +666,7 @@ def run_batch_parallel(model: NetworkModel, inputs: FeatureBatch, config: Infere
     if prepared is None:
         prepared = engine.prepare_model(model, config, mode)
     engine._check_prepared(prepared, model, mode)
-    distributed = torch.distributed.is_available() and torch.distributed.is_initialized()
-    w = torch.distributed.get_world_size() if distributed else config.workers
-    if distributed and w != config.workers:
-        raise ModelError(f"config.workers={config.workers} but world size is {w}")
-    dev = torch.device("cuda", torch.cuda.current_device())
     net = engine.device_network(prepared, model.bias)
-    bounds = shard_bounds(inputs.active_count, w)
-    m_cap = max((hi - lo for lo, hi in bounds), default=0)
-    transport = DistTransport(latency_hook, dev) if distributed else \
-        LocalTransport(w, latency_hook)
     cache = []
 
     def unpadded():
@@ -684,17 +674,54 @@ def run_batch_parallel(model: NetworkModel, inputs: FeatureBatch, config: Infere
             cache.append(engine.DeviceNetwork(engine._unpadded(prepared, model), model.bias))
         return cache[0]
 
+    return run_batch_parallel_device(net, inputs, config, latency_hook=latency_hook,
+                                     values=values, edges_per_input=count_edges(model),
+                                     unpadded=unpadded)
+
+
+def run_batch_parallel_device(net, inputs: FeatureBatch, config: InferenceConfig,
+                              latency_hook: LatencyHook | None = None, values: bool = True,
+                              edges_per_input: int | None = None, unpadded=None,
+                              shard_only: bool = False):
+    """run_batch_parallel on a network already resident in HBM (extension, the
+    counterpart of engine.infer_device): e.g. one built chunk by chunk with
+    DeviceNetwork.from_layers. ``shard_only`` (torch.distributed only): the
+    batch is the full 0..total_inputs-1 set and ``inputs`` holds just this
+    rank's partition_even shard of it, so no rank materialises the rest."""
+    import torch
+    from . import engine
+
+    if inputs.neurons != net.neurons:
+        raise ModelError("inputs do not match model width")
+    distributed = torch.distributed.is_available() and torch.distributed.is_initialized()
+    w = torch.distributed.get_world_size() if distributed else config.workers
+    if distributed and w != config.workers:
+        raise ModelError(f"config.workers={config.workers} but world size is {w}")
+    total = inputs.total_inputs
+    if shard_only and not distributed:
+        raise ModelError("shard_only needs a torch.distributed process group")
+    bounds = shard_bounds(total if shard_only else inputs.active_count, w)
+    m_cap = max((hi - lo for lo, hi in bounds), default=0)
+    transport = DistTransport(latency_hook, net.bias.device) if distributed else \
+        LocalTransport(w, latency_hook)
     shards = {}
+    data = np.asarray(inputs.data)
     for r in transport.local:
         lo, hi = bounds[r]
-        sh = DeviceShard(net, model.neurons, m_cap, model.num_layers, unpadded=unpadded)
-        x = torch.from_numpy(np.ascontiguousarray(np.asarray(inputs.data)[:, lo:hi].T))
-        sh.load(x, torch.from_numpy(np.ascontiguousarray(inputs.categories[lo:hi])))
+        cols = slice(lo, hi)
+        if shard_only:
+            if inputs.active_count != hi - lo or (hi > lo and (
+                    inputs.categories[0] != lo or inputs.categories[-1] != hi - 1)):
+                raise ModelError("inputs are not this rank's shard of the batch")
+            cols = slice(0, hi - lo)
+        sh = DeviceShard(net, net.neurons, m_cap, net.num_layers, unpadded=unpadded)
+        x = torch.from_numpy(np.ascontiguousarray(data[:, cols].T))
+        sh.load(x, torch.from_numpy(np.ascontiguousarray(inputs.categories[cols])))
         shards[r] = sh
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     totals, comm, balance, parts = run_layers_parallel(
-        model.num_layers, shards, transport, config.rebalance_threshold, w, values=values)
+        net.num_layers, shards, transport, config.rebalance_threshold, w, values=values)
     torch.cuda.synchronize()
     elapsed = time.perf_counter() - t0
     cats = torch.cat([p[0] for p in parts]).cpu().numpy().astype(np.int64)
@@ -705,8 +732,8 @@ def run_batch_parallel(model: NetworkModel, inputs: FeatureBatch, config: Infere
     final = None
     if values:
         vals = torch.cat([p[1] for p in parts]).cpu().numpy()[order]
-        final = FeatureBatch(neurons=model.neurons, data=vals.T, categories=cats,
-                             total_inputs=inputs.total_inputs)
+        final = FeatureBatch(neurons=net.neurons, data=vals.T, categories=cats,
+                             total_inputs=total)
     per_layer = []
     for l, (before, after) in enumerate(totals):
         if before == 0:
@@ -716,7 +743,7 @@ def run_batch_parallel(model: NetworkModel, inputs: FeatureBatch, config: Infere
             active_before=before, active_after=after,
             weight_element_reads=net.total_slots[l] * -(-before // engine.TILE),
             feature_element_reads=net.num_fp[l] * before))
+    epi = edges_per_input if edges_per_input is not None else int(sum(net.nnz))
     result = engine.InferenceResult(final=final, categories=cats.copy(), per_layer=per_layer,
-                                    elapsed_seconds=elapsed,
-                                    edges_processed=inputs.total_inputs * count_edges(model))
+                                    elapsed_seconds=elapsed, edges_processed=total * epi)
     return result, comm, balance

@@ -281,3 +281,81 @@ def test_config3_full_network_sampled_columns(cuda_ok):
     assert 0 < len(got) < len(pick)  # partial survival at density = |bias|
     pos = np.searchsorted(res.categories, ref.categories)
     assert same_bits(np.asarray(res.final.data)[:, pos], ref.final)
+
+
+def _streaming_case(layers=40, m=1500, bias=-0.3, seed=4):
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=layers, connections_per_neuron=32, bias_value=bias, seed=seed))
+    inputs = ingest.generate_synthetic_inputs(1024, m, 0.3, seed=seed + 1)
+    return model, inputs
+
+
+def _spy_streamer(monkeypatch):
+    captured = {}
+    orig = engine.WeightStreamer
+
+    class Spy(orig):
+        def __init__(self, *a, **k):
+            super().__init__(*a, **k)
+            captured["streamer"] = self
+
+    monkeypatch.setattr(engine, "WeightStreamer", Spy)
+    return captured
+
+
+def test_streaming_equals_resident(cuda_ok, monkeypatch):
+    """config.streaming (the reference's WeightStreamer path, engine.py:173-282):
+    identical categories, values and per-layer counts; at most two layers'
+    structures resident; every layer materialized once."""
+    model, inputs = _streaming_case()
+    eager = engine.infer(model, inputs, InferenceConfig())
+    captured = _spy_streamer(monkeypatch)
+    streamed = engine.infer(model, inputs, InferenceConfig(streaming=True))
+    st = captured["streamer"]
+    assert 1 <= st.peak_resident <= 2
+    assert st.materialized_count == 40
+    assert np.array_equal(streamed.categories, eager.categories)
+    assert same_bits(streamed.final.data, eager.final.data)
+    assert [(o.active_before, o.active_after) for o in streamed.per_layer] == \
+        [(o.active_before, o.active_after) for o in eager.per_layer]
+    ref = oracle.infer(model, inputs, threads=4)
+    assert streamed.categories.tolist() == ref.categories.tolist()
+    with pytest.raises(ModelError):
+        engine.infer(model, inputs, InferenceConfig(streaming=True),
+                     prepared=engine.prepare_model(model, InferenceConfig(), "optimized"))
+
+
+def test_streaming_stops_early_on_die_off(cuda_ok, monkeypatch):
+    """Every feature dead after a few layers: the streamer is stopped and the
+    remaining layers are never materialized (engine.py:265-270)."""
+    model, inputs = _streaming_case(layers=300, m=400, bias=-3.0)
+    captured = _spy_streamer(monkeypatch)
+    res = engine.infer(model, inputs, InferenceConfig(streaming=True))
+    assert len(res.categories) == 0
+    assert len(res.per_layer) == 300 and res.per_layer[-1].active_before == 0
+    assert captured["streamer"].materialized_count < 300
+    eager = engine.infer(model, inputs, InferenceConfig())
+    assert [(o.active_before, o.active_after) for o in res.per_layer] == \
+        [(o.active_before, o.active_after) for o in eager.per_layer]
+
+
+def test_chunked_device_network_infer_device(cuda_ok):
+    """DeviceNetwork.from_layers (plans built and uploaded a chunk of layers at
+    a time from a layer iterator) + infer_device == infer on the whole model."""
+    spec = ingest.GeneratorSpec(neurons=1024, layers=23, connections_per_neuron=32,
+                                bias_value=-0.3, seed=8)
+    model = ingest.generate_synthetic_network(spec)
+    inputs = ingest.generate_synthetic_inputs(1024, 900, 0.3, seed=9)
+    seen = []
+    net = engine.DeviceNetwork.from_layers(ingest.iter_synthetic_layers(spec),
+                                           ingest.synthetic_bias(spec), chunk=5,
+                                           on_chunk=lambda l0, lays: seen.append((l0, len(lays))))
+    assert seen == [(0, 5), (5, 5), (10, 5), (15, 5), (20, 3)]
+    assert net.num_layers == 23 and len(net.chunks) == 5
+    got = engine.infer_device(net, inputs)
+    want = engine.infer(model, inputs, InferenceConfig())
+    assert got.edges_processed == want.edges_processed
+    assert np.array_equal(got.categories, want.categories)
+    assert same_bits(got.final.data, want.final.data)
+    assert [(o.active_before, o.active_after) for o in got.per_layer] == \
+        [(o.active_before, o.active_after) for o in want.per_layer]
