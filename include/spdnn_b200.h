@@ -62,6 +62,8 @@ typedef struct spdnn_plan_params {
   int32_t max_groups;       /* max row groups per block (<= warps per CTA) */
   int32_t record_cap;       /* max union records staged per block stage */
   int32_t reorder;          /* 1 = order rows by column overlap, 0 = identity */
+  int32_t uniform_records;  /* 1 = when every stored weight has the same nonzero
+                               bits, one-word mask records (see export) */
 } spdnn_plan_params;
 
 typedef struct spdnn_plan spdnn_plan; /* opaque host plan for one layer */
@@ -70,7 +72,7 @@ typedef struct spdnn_plan spdnn_plan; /* opaque host plan for one layer */
 typedef struct spdnn_plan_sizes_t {
   int64_t neurons;
   int32_t rows_per_group;   /* R actually used */
-  int32_t record_words;     /* 32-bit words per union record (2, 4 or 8) */
+  int32_t record_words;     /* 32-bit words per union record (1, 2, 4 or 8) */
   int64_t num_blocks;
   int64_t num_extra_stages; /* stages beyond the first of multi-stage blocks */
   int64_t num_groups;
@@ -87,6 +89,8 @@ typedef struct spdnn_plan_sizes_t {
   int32_t pow2;             /* 1: every nonzero weight is +-2^e (FMA form allowed) */
   int32_t wexp_min;         /* exponent range of the nonzero weights */
   int32_t wexp_max;
+  int32_t uniform;          /* 1: mask records, every nonzero weight == weight_bits */
+  uint32_t weight_bits;
 } spdnn_plan_sizes_t;
 
 /* Build the plan for one CSR layer (canonical CSR as in model.py:35-58).
@@ -117,7 +121,11 @@ int spdnn_plan_sizes(const spdnn_plan *plan, spdnn_plan_sizes_t *sizes);
  *   records uint32[num_records * record_words]
  *           word 0 = smem byte offset of the input neuron's staged row
  *           (slot * SPDNN_STAGED_ROW_BYTES), words 1..R = fp32 weight bits
- *           per group row (0 = not connected); per group ascending neuron
+ *           per group row (0 = not connected); per group ascending neuron.
+ *           Uniform layers (sizes.uniform): one word per record,
+ *           slot << 24 | mask (bit k = group row k connects; the weight is
+ *           sizes.weight_bits), each group's run padded with zero words to a
+ *           multiple of 4
  */
 int spdnn_plan_export(const spdnn_plan *plan, int32_t *blocks, int32_t *stages,
                       int32_t *meta, uint32_t *records);
@@ -139,6 +147,8 @@ typedef struct spdnn_layer_dev {
   int32_t max_records_per_stage;
   int32_t max_meta_per_block;
   int32_t max_groups_per_block;  /* work units (row groups) per item */
+  int32_t uniform;               /* mask records (record_words == 1) */
+  uint32_t weight_bits;          /* the weight of every connection when uniform */
 } spdnn_layer_dev;
 
 /* Per-inference scratch shared by every layer launch (device pointers). */

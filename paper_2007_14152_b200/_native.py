@@ -31,7 +31,7 @@ i32, i64 = ctypes.c_int32, ctypes.c_int64
 
 class PlanParams(ctypes.Structure):
     _fields_ = [("rows_per_group", i32), ("footprint_cap", i32), ("max_groups", i32),
-                ("record_cap", i32), ("reorder", i32)]
+                ("record_cap", i32), ("reorder", i32), ("uniform_records", i32)]
 
 
 class PlanSizes(ctypes.Structure):
@@ -41,14 +41,16 @@ class PlanSizes(ctypes.Structure):
                 ("padded_slots", i64), ("max_fp_per_stage", i32),
                 ("max_records_per_stage", i32), ("max_meta_per_block", i32),
                 ("max_groups_per_block", i32), ("pow2", i32),
-                ("wexp_min", i32), ("wexp_max", i32)]
+                ("wexp_min", i32), ("wexp_max", i32), ("uniform", i32),
+                ("weight_bits", ctypes.c_uint32)]
 
 
 class LayerDev(ctypes.Structure):
     _fields_ = [("blocks", P), ("stages", P), ("meta", P), ("records", P),
                 ("num_blocks", i64), ("neurons", i64), ("rows_per_group", i32),
                 ("record_words", i32), ("max_fp_per_stage", i32), ("max_records_per_stage", i32),
-                ("max_meta_per_block", i32), ("max_groups_per_block", i32)]
+                ("max_meta_per_block", i32), ("max_groups_per_block", i32),
+                ("uniform", i32), ("weight_bits", ctypes.c_uint32)]
 
 
 class Scratch(ctypes.Structure):

@@ -49,7 +49,10 @@
 
 namespace {
 
-constexpr int kMaxBufs = 4;  // ring depth: as many buffers as shared memory holds (<= 4)
+constexpr int kMaxBufs = 4;
+#ifndef SPDNN_MASK_CONSUMERS
+#define SPDNN_MASK_CONSUMERS 20
+#endif  // ring depth: as many buffers as shared memory holds (<= 4)
 constexpr int kHeaderBytes = 128;  // keeps every region 128-byte aligned (TMA dst)
 
 typedef unsigned long long u64;
@@ -249,22 +252,29 @@ struct Rec<7> {
 // a staged input neuron is a (128 * FPL)-byte smem row. FPL = 4 reuses every
 // weight over more features, FPL = 2 halves the accumulator registers and
 // buys twice the resident consumer warps.
-template <int FPL>
+// MASK = one-word mask records (uniform weights): no weight registers per
+// record in flight, so the consumer loop fits 80 registers and 20 consumer
+// warps (6 warps per scheduler instead of 5) hide the smem latency better.
+template <int FPL, bool MASK>
 struct Cfg;
 template <>
-struct Cfg<4> {
-  static constexpr int kConsumers = 16, kProducers = 4, kMaxRegs = 96;
+struct Cfg<4, false> {
+  static constexpr int kConsumers = 16, kProducers = 4;
 };
 template <>
-struct Cfg<2> {
-  static constexpr int kConsumers = 28, kProducers = 4, kMaxRegs = 64;
+struct Cfg<4, true> {
+  static constexpr int kConsumers = SPDNN_MASK_CONSUMERS, kProducers = 4;
 };
-template <int FPL>
+template <bool MASK>
+struct Cfg<2, MASK> {
+  static constexpr int kConsumers = 28, kProducers = 4;
+};
+template <int FPL, bool MASK = false>
 struct Geo {
   static constexpr int kTileF = 32 * FPL;      // features per item
   static constexpr int kRow = 4 * kTileF;      // staged row bytes
-  static constexpr int kC = Cfg<FPL>::kConsumers;
-  static constexpr int kP = Cfg<FPL>::kProducers;
+  static constexpr int kC = Cfg<FPL, MASK>::kConsumers;
+  static constexpr int kP = Cfg<FPL, MASK>::kProducers;
   static constexpr int kThreads = (kC + kP) * 32;
   // record offsets are slot * SPDNN_STAGED_ROW_BYTES (512): shift to this row size
   static constexpr int kOffShift = FPL == 4 ? 0 : 1;
@@ -280,11 +290,18 @@ struct YVec<4> {
     v[0] = t.x;
     v[1] = t.y;
   }
+  // from a 32-bit shared-window address (one LEA.HI forms it from a record)
+  __device__ __forceinline__ void load_s(uint32_t a) {
+    asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "r"(a));
+  }
 };
 template <>
 struct YVec<2> {
   u64 v[1];
   __device__ __forceinline__ void load(const char *p) { v[0] = *reinterpret_cast<const u64 *>(p); }
+  __device__ __forceinline__ void load_s(uint32_t a) {
+    asm("ld.shared.u64 %0, [%1];" : "=l"(v[0]) : "r"(a));
+  }
 };
 
 // acc[(FPL/2)*k + h]: row k, features (FPL*l + 2h, FPL*l + 2h + 1).
@@ -307,6 +324,40 @@ __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int c
       for (int h = 0; h < H; h++) {
         if (FMA) fma2_acc(acc[H * k + h], y.v[h], w[k]);
         else mul_add2_acc(acc[H * k + h], y.v[h], w[k], negz2);
+      }
+    }
+  }
+}
+
+// Mask records (uniform weight w): 4 one-word records per 16-byte load; word
+// = staged-row slot << 24 | row mask, so the row's byte offset is word >> 15
+// (one LEA.HI with the base). Rows whose bit is clear add nothing --
+// exactly the reference's sum, which never visits those columns. Each
+// group's run is padded to a multiple of 4 with zero words (no-ops).
+template <int R, bool FMA, int FPL>
+__device__ __forceinline__ void accumulate_mask(u64 *acc, const uint32_t *recs, int cnt,
+                                                uint32_t ybase, float w, u64 negz2) {
+  constexpr int H = FPL / 2;
+  const uint4 *rp = reinterpret_cast<const uint4 *>(recs);
+  const uint4 *const end = rp + (cnt >> 2);
+#pragma unroll 2
+  for (; rp < end; rp++) {
+    const uint4 q = *rp;
+    const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+    YVec<FPL> y[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) y[j].load_s(ybase + (wd[j] >> (15 + Geo<FPL>::kOffShift)));
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+#pragma unroll
+      for (int k = 0; k < R; k++) {
+        if (wd[j] & (1u << k)) {
+#pragma unroll
+          for (int h = 0; h < H; h++) {
+            if (FMA) fma2_acc(acc[H * k + h], y[j].v[h], w);
+            else mul_add2_acc(acc[H * k + h], y[j].v[h], w, negz2);
+          }
+        }
       }
     }
   }
@@ -431,10 +482,11 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int
 // Extra stages of a lone oversized group (rare: a row group whose inputs
 // exceed the staging caps): its records are consumed straight from global
 // memory, the feature values gathered through a_in. Slow, correct.
-template <int R, bool FMA, int FPL>
+template <int R, bool FMA, int FPL, bool MASK>
 __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, int lane, int M,
                                   u64 negz2) {
-  constexpr int RW = Rec<R>::W, H = FPL / 2, T = Geo<FPL>::kTileF;
+  constexpr int RW = MASK ? 1 : Rec<R>::W, H = FPL / 2, T = Geo<FPL>::kTileF;
+  const float w0 = __uint_as_float(A.L.weight_bits);
   const int nst = __ldg(A.L.blocks + (int64_t)b * 8 + 2);
   const int first_extra = __ldg(A.L.blocks + (int64_t)b * 8 + 3);
   int pos[FPL];
@@ -451,7 +503,15 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
     for (int i = 0; i < sd.w; i++) {
       uint32_t off;
       float w[R];
-      Rec<R>::load(recs + i * RW, off, w);  // (global loads)
+      if (MASK) {
+        const uint32_t wd = __ldg(recs + i);
+        off = wd >> 15;
+#pragma unroll
+        for (int k = 0; k < R; k++) w[k] = (wd >> k) & 1u ? w0 : 0.0f;
+        if ((wd & ((1u << R) - 1u)) == 0u) continue;  // padding word
+      } else {
+        Rec<R>::load(recs + i * RW, off, w);  // (global loads)
+      }
       const int64_t c = __ldg(A.L.meta + sd.x + off / SPDNN_STAGED_ROW_BYTES);
       const float *row = A.y_in + c * A.ld;
       float v[FPL];
@@ -462,6 +522,7 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
         const u64 y = pack2(v[2 * h], v[2 * h + 1]);
 #pragma unroll
         for (int k = 0; k < R; k++) {
+          if (MASK && w[k] == 0.0f) continue;  // row not connected: no term
           if (FMA) fma2_acc(acc[H * k + h], y, w[k]);
           else mul_add2_acc(acc[H * k + h], y, w[k], negz2);
         }
@@ -470,17 +531,18 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
   }
 }
 
-template <int R, bool FMA, int FPL>
-__global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
+template <int R, bool FMA, int FPL, bool MASK>
+__global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ int s_done[kMaxBufs];
   __shared__ int s_pitem[2];
+  __shared__ float s_wmask;
 
-  using G = Geo<FPL>;
-  constexpr int RW = Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
+  using G = Geo<FPL, MASK>;
+  constexpr int RW = MASK ? 1 : Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int M = *A.m_in;
   if (M <= 0) return;
@@ -493,6 +555,7 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
   const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(&s_empty[0]);
 
   if (tid == 0) {
+    s_wmask = __uint_as_float(A.L.weight_bits);
     for (int i = 0; i < nbuf; i++) {
       mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
       mbar_init(empty0 + 8 * i, gpi);  // one arrival per work unit (row group) of the item
@@ -672,6 +735,10 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
   // <= nbuf apart, so the slot's barrier may still be one phase behind: the
   // header's entry number tells a stale phase from the awaited one.
   const u64 negz2 = pack2(A.negz, A.negz);
+  // the uniform weight, read from shared memory once: taken from the kernel
+  // parameter, ptxas re-loads it from the constant bank before every
+  // predicated FFMA2 instead of keeping it in a register
+  const float w_mask = s_wmask;
   // unit u = warp + j*C  ->  (entry k, group g, ring slot, phase), advanced
   // incrementally (no per-unit integer division)
   int k = warp / gpi, g = warp - (warp / gpi) * gpi;
@@ -697,6 +764,21 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
       const uint32_t *recs = reinterpret_cast<const uint32_t *>(buf + kHeaderBytes + A.meta_bytes);
       const char *ybase = buf + kHeaderBytes + A.meta_bytes + A.rec_bytes + 4 * FPL * lane;
       const int seg_base = (h.fp_cnt + 3) & ~3;
+      u64 acc[H * R];
+#pragma unroll
+      for (int r = 0; r < H * R; r++) acc[r] = 0ull;
+      if (MASK) {
+        accumulate_mask<R, FMA, FPL>(acc, recs + meta[seg_base + 2 * g],
+                                     meta[seg_base + 2 * g + 1],
+                                     (uint32_t)__cvta_generic_to_shared(ybase), w_mask, negz2);
+      } else {
+        accumulate<R, FMA, FPL, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
+                                   meta[seg_base + 2 * g + 1], ybase, negz2);
+      }
+      if (h.nst > 1) accumulate_global<R, FMA, FPL, MASK>(A, acc, h.b, h.t, lane, M, negz2);
+      // output rows and their biases (staged with the block metadata) are read
+      // only now, so they hold no registers across the record loop
+      asm volatile("" ::: "memory");
       int rows[R];
       float bias[R];
       const int *mrows = meta + seg_base + 2 * h.ng + R * g;
@@ -704,14 +786,8 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
 #pragma unroll
       for (int r = 0; r < R; r++) {
         rows[r] = mrows[r];
-        bias[r] = mbias[r];  // bias[row] staged with the block metadata
+        bias[r] = mbias[r];
       }
-      u64 acc[H * R];
-#pragma unroll
-      for (int r = 0; r < H * R; r++) acc[r] = 0ull;
-      accumulate<R, FMA, FPL, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
-                                 meta[seg_base + 2 * g + 1], ybase, negz2);
-      if (h.nst > 1) accumulate_global<R, FMA, FPL>(A, acc, h.b, h.t, lane, M, negz2);
       epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
     }
     __syncwarp();
@@ -787,16 +863,17 @@ __global__ void __launch_bounds__(Geo<FPL>::kThreads, 1)
 
 // ---- launch configuration ---------------------------------------------------
 
-template <int R, int FPL>
+template <int R, int FPL, bool MASK>
 void *kernel_ptr(bool fma) {
-  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true, FPL>)
-             : reinterpret_cast<void *>(&layer_kernel<R, false, FPL>);
+  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true, FPL, MASK>)
+             : reinterpret_cast<void *>(&layer_kernel<R, false, FPL, MASK>);
 }
 
-template <int FPL>
+template <int FPL, bool MASK>
 void *kernel_for(int R, bool fma) {
-  return R == 1 ? kernel_ptr<1, FPL>(fma)
-                : (R == 3 ? kernel_ptr<3, FPL>(fma) : (R == 7 ? kernel_ptr<7, FPL>(fma) : nullptr));
+  return R == 1 ? kernel_ptr<1, FPL, MASK>(fma)
+                : (R == 3 ? kernel_ptr<3, FPL, MASK>(fma)
+                          : (R == 7 ? kernel_ptr<7, FPL, MASK>(fma) : nullptr));
 }
 
 struct DevInfo {
@@ -823,12 +900,14 @@ int device_info(int &sms, size_t &optin) {
   return 0;
 }
 
-template <int FPL>
+template <int FPL, bool MASK>
 int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
-  using G = Geo<FPL>;
+  using G = Geo<FPL, MASK>;
   const spdnn_layer_dev &L = A.L;
-  void *fn = kernel_for<FPL>(L.rows_per_group, fma);
+  void *fn = kernel_for<FPL, MASK>(L.rows_per_group, fma);
   if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1, 3 or 7");
+  if (MASK != (L.uniform != 0) || (MASK && L.record_words != 1))
+    return spdnn_fail(SPDNN_EINVAL, "layer: record format does not match the layout");
   int sms;
   size_t optin;
   if (device_info(sms, optin)) return spdnn_fail(SPDNN_ECUDA, "layer: no CUDA device");
@@ -1006,8 +1085,10 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   std::memcpy(&tb, &A.tiny, 4);
   A.tiny_bits_m1 = tb ? tb - 1u : 0u;
   A.negz = -0.0f;
-  return fpl == 2 ? launch_layer<2>(A, fma, (cudaStream_t)stream)
-                  : launch_layer<4>(A, fma, (cudaStream_t)stream);
+  const bool mask = layer->uniform != 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (fpl == 2) return mask ? launch_layer<2, true>(A, fma, st) : launch_layer<2, false>(A, fma, st);
+  return mask ? launch_layer<4, true>(A, fma, st) : launch_layer<4, false>(A, fma, st);
 }
 
 }  // namespace
@@ -1065,7 +1146,7 @@ extern "C" int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int
 extern "C" int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_sm,
                                      int32_t *threads_per_cta) {
   (void)rows_per_group;
-  if (threads_per_cta) *threads_per_cta = Geo<4>::kThreads;
+  if (threads_per_cta) *threads_per_cta = Geo<4, true>::kThreads;
   if (ctas_per_sm) *ctas_per_sm = 1;
   return SPDNN_OK;
 }

@@ -45,12 +45,32 @@ struct spdnn_plan {
   int64_t union_records = 0;     // records excluding alignment padding
   int32_t pow2 = 0;              // every nonzero weight is +-2^e (FMA form allowed)
   int32_t wexp_min = 0, wexp_max = 0;
+  int32_t uniform = 0;           // one-word mask records: every nonzero has these bits
+  uint32_t weight_bits = 0;
 };
 
 namespace {
 
 
-int record_words(int R) { return R == 1 ? 2 : (R == 3 ? 4 : 8); }
+int record_words(int R, bool uniform) {
+  return uniform ? 1 : (R == 1 ? 2 : (R == 3 ? 4 : 8));
+}
+
+// True when every stored weight has the same nonzero bit pattern: the layer
+// is then described by its pattern alone and a record is one 32-bit word,
+// staged-row slot << 24 | R-bit row mask (slots < 256: footprint_cap <= 256).
+// Graph Challenge layers are all 1/16.
+bool uniform_weights(int64_t nnz, const float *va, uint32_t &bits) {
+  if (nnz == 0) return false;
+  std::memcpy(&bits, &va[0], 4);
+  if ((bits & 0x7fffffffu) == 0) return false;
+  for (int64_t p = 1; p < nnz; p++) {
+    uint32_t b;
+    std::memcpy(&b, &va[p], 4);
+    if (b != bits) return false;
+  }
+  return true;
+}
 
 bool valid_csr(int64_t n, const int64_t *rp, const int32_t *ci) {
   if (n < 0 || rp[0] != 0) return false;
@@ -180,6 +200,10 @@ int64_t total_records(const std::vector<Group> &gs) {
 // R=1: 4 issue, 3 wavefronts; R=3: 8 issue, 3 wavefronts; R=7: 17 issue,
 // 4 wavefronts. Time ~ max(issue/4, wavefronts) smem-or-issue bound per SM.
 double record_cost(int R) { return R == 1 ? 3.0 : (R == 3 ? 3.0 : 4.25); }
+// Mask records (uniform weights), SM clocks per record: the staged-row load
+// is 4 smem wavefronts plus a quarter of a broadcast record load; the FMA
+// pipe retires 2 FFMA2 per clock per SM (R = 7: 14 FFMA2 = 7 clocks).
+double mask_record_cost(int R) { return R == 7 ? 7.0 : 4.25; }
 
 void pad4(std::vector<int32_t> &v) {
   while (v.size() % 4) v.push_back(0);
@@ -220,16 +244,27 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
         if (c < lo_col || c > hi_col) continue;
         const size_t base = pl->records.size();
         pl->records.resize(base + RW, 0u);
-        pl->records[base] = (uint32_t)slot_of[c] * (uint32_t)SPDNN_STAGED_ROW_BYTES;
+        // generic: word 0 = byte offset of the staged row; mask records:
+        // slot << 24 | row mask (the kernel's address is base + word >> 15)
+        pl->records[base] = pl->uniform ? (uint32_t)slot_of[c] << 24
+                                        : (uint32_t)slot_of[c] * (uint32_t)SPDNN_STAGED_ROW_BYTES;
         for (int k = 0; k < R; k++) {
           const int32_t row = gs[gg].rows[k];
           const float w = row >= 0 ? weight(row, c) : 0.0f;
           uint32_t bits;
           std::memcpy(&bits, &w, 4);
-          pl->records[base + 1 + k] = bits;
+          if (pl->uniform) pl->records[base] |= (bits != 0u ? 1u : 0u) << k;
+          else pl->records[base + 1 + k] = bits;
         }
         cnt++;
       }
+      // mask records: each group's run padded to a multiple of 4 (the kernel
+      // reads 4 records per 16-byte load); padding words are mask 0 (no-op)
+      if (pl->uniform)
+        while (cnt % 4) {
+          pl->records.push_back(0u);
+          cnt++;
+        }
       if (gseg) {
         gseg->push_back((int32_t)start);
         gseg->push_back((int32_t)cnt);
@@ -330,6 +365,11 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
   pl->n = n;
   pl->nnz = n > 0 ? row_ptr[n] : 0;
   try {
+    uint32_t wb = 0;
+    if (p.uniform_records && p.footprint_cap <= 256 && uniform_weights(pl->nnz, values, wb)) {
+      pl->uniform = 1;
+      pl->weight_bits = wb;
+    }
     std::vector<int32_t> ident(n);
     for (int64_t i = 0; i < n; i++) ident[i] = (int32_t)i;
     int R = p.rows_per_group;
@@ -345,14 +385,15 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
         double best_cost = 0;
         for (int cand : {1, 3, 7}) {
           auto gs = make_groups(n, row_ptr, col_idx, cand == 1 ? ident : order, cand);
-          double cost = (double)total_records(gs) * record_cost(cand);
+          double cost = (double)total_records(gs) *
+                        (pl->uniform ? mask_record_cost(cand) : record_cost(cand));
           if (best.empty() && cand == 1) { best = std::move(gs); R = 1; best_cost = cost; continue; }
           if (cost < best_cost) { best = std::move(gs); R = cand; best_cost = cost; }
         }
       }
     }
     pl->R = R;
-    pl->RW = record_words(R);
+    pl->RW = record_words(R, pl->uniform != 0);
     pl->num_groups = (int64_t)best.size();
     pl->pow2 = pow2_weights(pl->nnz, values, pl->wexp_min, pl->wexp_max) ? 1 : 0;
     emit(pl, row_ptr, col_idx, values, best, p);
@@ -423,6 +464,8 @@ extern "C" int spdnn_plan_sizes(const spdnn_plan *pl, spdnn_plan_sizes_t *s) {
   s->pow2 = pl->pow2;
   s->wexp_min = pl->wexp_min;
   s->wexp_max = pl->wexp_max;
+  s->uniform = pl->uniform;
+  s->weight_bits = pl->weight_bits;
   return SPDNN_OK;
 }
 

@@ -77,6 +77,7 @@ class PlanParams:
     max_groups: int = 16         # row groups per block (one per warp)
     record_cap: int = 640        # union records per block stage
     reorder: bool = True
+    uniform_records: bool = True  # one-word mask records when all weights are equal
 
 
 BASELINE_PARAMS = PlanParams(rows_per_group=1, reorder=False)
@@ -109,6 +110,8 @@ class LayerPlan:
     num_records: int
     num_fp: int
     padded_slots: int
+    uniform: bool          # one-word mask records; every connection weighs weight_bits
+    weight_bits: int
     blocks: np.ndarray    # int32 [num_blocks, 8] descriptors
     stages: np.ndarray    # int32 [num_extra_stages, 4]
     meta: np.ndarray      # int32 per-block fp lists / group segments / rows
@@ -130,7 +133,7 @@ class PreparedLayer:
 
 def _params_struct(p: PlanParams) -> _native.PlanParams:
     return _native.PlanParams(p.rows_per_group, p.footprint_cap, p.max_groups, p.record_cap,
-                              int(p.reorder))
+                              int(p.reorder), int(p.uniform_records))
 
 
 def _export(handle) -> LayerPlan:
@@ -155,7 +158,8 @@ def _export(handle) -> LayerPlan:
                      max_meta_per_block=s.max_meta_per_block,
                      max_groups_per_block=s.max_groups_per_block,
                      num_records=s.num_records, num_fp=s.num_fp,
-                     padded_slots=s.padded_slots, **arrs)
+                     padded_slots=s.padded_slots, uniform=bool(s.uniform),
+                     weight_bits=int(s.weight_bits), **arrs)
 
 
 def _padding(layer: LayerCSR, plan: LayerPlan) -> PaddingStats:
@@ -371,6 +375,8 @@ class DeviceNetwork:
             d.max_records_per_stage = pl.max_records_per_stage
             d.max_meta_per_block = pl.max_meta_per_block
             d.max_groups_per_block = pl.max_groups_per_block
+            d.uniform = int(pl.uniform)
+            d.weight_bits = pl.weight_bits
         self._plans_meta = [None] * self.num_layers  # host arrays no longer needed
         # FMA form (one FFMA2 per (row, column)) is exact when every weight is
         # +-2^e and no input falls below `tiny` (products stay normal) or above

@@ -1,5 +1,6 @@
 """CPU re-execution of a LayerPlan in the exact order and rounding the CUDA
-kernel uses (csrc/layer.cu). Test infrastructure: lets the layout builder be
+kernel uses (csrc/layer.cu), for both record formats (per-row weights, and
+the one-word mask records of uniform-weight layers). Test infrastructure: lets the layout builder be
 checked bit-for-bit against the oracle without a GPU. float32 numpy ops are
 IEEE single precision with round-to-nearest, like the kernel's fma.rn with
 an exact product / add.rn."""
@@ -52,6 +53,15 @@ def emulate_layer(plan, bias, x):
             for s, rel, cnt in segs:
                 fp, recs = stages[s]
                 for r in recs[rel:rel + cnt]:
+                    if plan.uniform:
+                        # one word: slot << 24 | row mask; unset bits add nothing
+                        word = int(r[0])
+                        y = x[fp[word >> 24]]
+                        w = np.uint32(plan.weight_bits).view(np.float32)
+                        for k in range(R):
+                            if word >> k & 1:
+                                acc[k] = acc[k] + (y * w).astype(np.float32)
+                        continue
                     assert int(r[0]) % ROW_BYTES == 0
                     y = x[fp[int(r[0]) // ROW_BYTES]]
                     ws = r[1:1 + R].view(np.float32)

@@ -129,3 +129,33 @@ def test_prepare_model_modes_and_stats():
         assert p.padding.padded_slots >= p.padding.nnz
     with pytest.raises(ModelError):
         engine.prepare_model(model, cfg, "fast")
+
+
+def test_uniform_weight_layers_use_mask_records():
+    """All stored weights identical (every Graph Challenge layer): one-word
+    mask records, each group's run padded to 4; the same layer with the
+    format disabled, with a second weight value, or with an explicit zero
+    falls back to per-row weight records. All bit-exact."""
+    rng = np.random.default_rng(5)
+    spec = ingest.GeneratorSpec(neurons=200, layers=1, connections_per_neuron=12, seed=3)
+    layer = ingest.generate_synthetic_network(spec).layers[0]
+    for params in (PlanParams(), PlanParams(rows_per_group=3),
+                   PlanParams(rows_per_group=1, reorder=False),
+                   PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3)):
+        plan = _check(layer, params, rng)
+        assert plan.uniform and plan.record_words == 1
+        assert plan.weight_bits == 0x3D800000
+    plan = _check(layer, PlanParams(uniform_records=False), rng)
+    assert not plan.uniform and plan.record_words in (2, 4, 8)
+    neg = make_layer_csr(200, np.repeat(np.arange(200), np.diff(layer.row_ptr)),
+                         layer.col_idx, np.full(layer.nnz, -0.5, np.float32))
+    assert _check(neg, PlanParams(), rng).uniform
+    vals = layer.values.copy()
+    vals[17] = np.float32(0.125)
+    two = make_layer_csr(200, np.repeat(np.arange(200), np.diff(layer.row_ptr)),
+                         layer.col_idx, vals)
+    assert not _check(two, PlanParams(), rng).uniform
+    vals[17] = np.float32(0.0)
+    zero = make_layer_csr(200, np.repeat(np.arange(200), np.diff(layer.row_ptr)),
+                          layer.col_idx, vals)
+    assert not _check(zero, PlanParams(), rng).uniform
