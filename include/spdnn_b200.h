@@ -211,6 +211,13 @@ int spdnn_transpose_in(const float *x, int64_t n, int64_t m, float *y,
 int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int32_t *a,
                      const int64_t *perm, int64_t m, float *out, void *stream);
 
+/* Cycle accounting of the layer kernel when the library was built with
+ * -DSPDNN_PROFILE (all zero otherwise): out[0..7] consumer-warp clock64 sums
+ * (wait for data, record loop, epilogue, bookkeeping), out[8..15] producer
+ * warps (empty-slot wait, barrier A, copy issue, metadata, barrier B, tail).
+ * Diagnostics only. */
+int spdnn_profile_read(uint64_t *out, int32_t n, int32_t reset);
+
 /* Threadblocks per SM the layer kernel runs with (for diagnostics). */
 int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_sm,
                           int32_t *threads_per_cta);

@@ -75,7 +75,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
             return LIB_PATH
     os.makedirs(LIB_DIR, exist_ok=True)
     tmp = LIB_PATH + ".tmp"
-    cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-o", tmp, *srcs]
+    # SPDNN_NVCC_DEFINES: extra -D flags for tuning sweeps (e.g.
+    # "-DSPDNN_MASK_CONSUMERS=16"); the default build sets none
+    extra = os.environ.get("SPDNN_NVCC_DEFINES", "").split()
+    cmd = ["nvcc", *NVCC_FLAGS, *extra, "-I", INCLUDE, "-o", tmp, *srcs]
     res = subprocess.run(cmd, capture_output=not verbose, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + (res.stderr or "") + (res.stdout or ""))
@@ -106,6 +109,8 @@ def lib():
         L.spdnn_transpose_in.argtypes = [P, i64, i64, P, i64, P, ctypes.c_float,
                                          ctypes.c_float, P]
         L.spdnn_gather_out.argtypes = [P, i64, i64, P, P, i64, P, P]
+        L.spdnn_profile_read.argtypes = [P, i32, i32]
+        L.spdnn_profile_read.restype = ctypes.c_int
         L.spdnn_last_error.restype = ctypes.c_char_p
         L.spdnn_version.restype = ctypes.c_char_p
         for name in ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
@@ -130,4 +135,5 @@ def check(rc: int, what: str) -> None:
 EXPORTED = ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
             "spdnn_plan_export", "spdnn_plan_free", "spdnn_layer_forward",
             "spdnn_infer_layers", "spdnn_transpose_in", "spdnn_gather_out",
-            "spdnn_layer_occupancy", "spdnn_last_error", "spdnn_version")
+            "spdnn_layer_occupancy", "spdnn_profile_read", "spdnn_last_error",
+            "spdnn_version")

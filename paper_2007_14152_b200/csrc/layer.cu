@@ -50,9 +50,18 @@
 namespace {
 
 constexpr int kMaxBufs = 4;
+constexpr int kMetaAhead = 4;  // producer metadata prefetch distance (items)
+constexpr int kMetaRing = 6;   // metadata ring entries (> kMetaAhead)
 #ifndef SPDNN_MASK_CONSUMERS
 #define SPDNN_MASK_CONSUMERS 20
-#endif  // ring depth: as many buffers as shared memory holds (<= 4)
+#endif
+#ifndef SPDNN_MASK_PRODUCERS
+#define SPDNN_MASK_PRODUCERS 3
+#endif
+#ifndef SPDNN_MASK_UNROLL
+#define SPDNN_MASK_UNROLL 2
+#endif
+constexpr int kMaskUnroll = SPDNN_MASK_UNROLL;  // 4-record quads per loop iteration  // ring depth: as many buffers as shared memory holds (<= 4)
 constexpr int kHeaderBytes = 128;  // keeps every region 128-byte aligned (TMA dst)
 
 typedef unsigned long long u64;
@@ -61,9 +70,6 @@ __device__ __forceinline__ u64 pack2(float a, float b) {
   u64 r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
   return r;
-}
-__device__ __forceinline__ void unpack2(u64 v, float &a, float &b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
 }
 // acc = y * w + acc in place. The CUDA intrinsic (not inline asm) lets the
 // register allocator keep each accumulator in place (inline-asm "+l" operands
@@ -84,18 +90,7 @@ __device__ __forceinline__ void mul_add2_acc(u64 &acc, u64 y, float w, u64 negz2
   a = __fadd2_rn(a, p);
   acc = *reinterpret_cast<u64 *>(&a);
 }
-__device__ __forceinline__ u64 add2(u64 a, u64 b) {
-  u64 r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 
-__device__ __forceinline__ float clamp32(float v) {
-  // comparison clamp in the reference's order; NaN falls through unchanged
-  v = (v < 0.0f) ? 0.0f : v;
-  v = (v > 32.0f) ? 32.0f : v;
-  return v;
-}
 
 // ---- async copy + mbarrier primitives -------------------------------------
 
@@ -103,26 +98,20 @@ __device__ __forceinline__ void cp_async4(uint32_t saddr, const void *gmem, bool
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(saddr), "l"(gmem),
                "r"(valid ? 4 : 0));
 }
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar)
                : "memory");
-}
-// One bounded wait (suspends up to ~2 us): true when the phase with `parity` is done.
-__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n"
-      " .reg .pred p;\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
-      " selp.u32 %0, 1, 0, p;\n"
-      "}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity), "r"(2000)
-      : "memory");
-  return ok != 0;
 }
 // Blocks (suspended, up to the time hint) until the phase with `parity` is done.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
@@ -166,6 +155,30 @@ __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32
       : "memory");
 }
 
+// ---- optional cycle accounting (build with -DSPDNN_PROFILE; diagnostics) ----
+// Per warp, clock64() spans between marks are summed into 8 slots and added to
+// g_prof at exit: consumers [0..7], producers [8..15]; read and reset with
+// spdnn_profile_read().
+__device__ unsigned long long g_prof[16];
+#ifdef SPDNN_PROFILE
+#define PROF_DECL                          \
+  unsigned long long pf_[8] = {0};         \
+  long long pt_ = clock64();
+#define PROF_MARK(i)                       \
+  {                                        \
+    const long long n_ = clock64();        \
+    pf_[i] += (unsigned long long)(n_ - pt_); \
+    pt_ = n_;                              \
+  }
+#define PROF_FLUSH(base)                   \
+  if (lane == 0)                           \
+    for (int i_ = 0; i_ < 8; i_++) atomicAdd(&g_prof[(base) + i_], pf_[i_]);
+#else
+#define PROF_DECL
+#define PROF_MARK(i)
+#define PROF_FLUSH(base)
+#endif
+
 struct LayerArgs {
   CUtensorMap tmap_in;  // y_in as a 2-D tensor [N rows][ld cols], box 128 x 1
   spdnn_layer_dev L;
@@ -190,6 +203,8 @@ struct LayerArgs {
   uint32_t meta_bytes;
   uint32_t rec_bytes;
   int nbuf;            // ring depth
+  uint32_t mring_off;  // producer metadata ring (after the nbuf buffers)
+  uint32_t mentry_bytes;
   int simple_wait;     // 1: consumer warps visit every (C/gpi)-th entry and (C/gpi) | nbuf
   int gpi;             // consumer work units (row groups) per item = max groups per block
 };
@@ -259,15 +274,15 @@ template <int FPL, bool MASK>
 struct Cfg;
 template <>
 struct Cfg<4, false> {
-  static constexpr int kConsumers = 16, kProducers = 4;
+  static constexpr int kConsumers = 16, kProducers = 3;
 };
 template <>
 struct Cfg<4, true> {
-  static constexpr int kConsumers = SPDNN_MASK_CONSUMERS, kProducers = 4;
+  static constexpr int kConsumers = SPDNN_MASK_CONSUMERS, kProducers = SPDNN_MASK_PRODUCERS;
 };
 template <bool MASK>
 struct Cfg<2, MASK> {
-  static constexpr int kConsumers = 28, kProducers = 4;
+  static constexpr int kConsumers = 28, kProducers = 3;
 };
 template <int FPL, bool MASK = false>
 struct Geo {
@@ -275,7 +290,7 @@ struct Geo {
   static constexpr int kRow = 4 * kTileF;      // staged row bytes
   static constexpr int kC = Cfg<FPL, MASK>::kConsumers;
   static constexpr int kP = Cfg<FPL, MASK>::kProducers;
-  static constexpr int kThreads = (kC + kP) * 32;
+  static constexpr int kThreads = (kC + kP + 1) * 32;  // + the publisher warp
   // record offsets are slot * SPDNN_STAGED_ROW_BYTES (512): shift to this row size
   static constexpr int kOffShift = FPL == 4 ? 0 : 1;
 };
@@ -340,7 +355,7 @@ __device__ __forceinline__ void accumulate_mask(u64 *acc, const uint32_t *recs, 
   constexpr int H = FPL / 2;
   const uint4 *rp = reinterpret_cast<const uint4 *>(recs);
   const uint4 *const end = rp + (cnt >> 2);
-#pragma unroll 2
+#pragma unroll kMaskUnroll
   for (; rp < end; rp++) {
     const uint4 q = *rp;
     const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
@@ -433,6 +448,9 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
       else if (rows[k] >= 0) mx[q] = fmaxf(mx[q], x[q]);
     }
     if (rows[k] < 0) continue;
+#ifdef SPDNN_ABLATE_STORE
+    if (rows[k] >= 0) continue;  // diagnostics: no output stores
+#endif
     float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
     if (FULL) {
       if (FPL == 4) *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
@@ -535,11 +553,10 @@ template <int R, bool FMA, int FPL, bool MASK>
 __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
-  __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs];
+  __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs], s_free[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
-  __shared__ int s_done[kMaxBufs];
-  __shared__ int s_pitem[2];
   __shared__ float s_wmask;
+  __shared__ int s_items[8];  // producer: item index of ring entry j (j & 7)
 
   using G = Geo<FPL, MASK>;
   constexpr int RW = MASK ? 1 : Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
@@ -553,20 +570,21 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
   const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(&s_empty[0]);
+  const uint32_t free0 = (uint32_t)__cvta_generic_to_shared(&s_free[0]);
 
   if (tid == 0) {
     s_wmask = __uint_as_float(A.L.weight_bits);
     for (int i = 0; i < nbuf; i++) {
       mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
       mbar_init(empty0 + 8 * i, gpi);  // one arrival per work unit (row group) of the item
-      s_done[i] = 0;
+      mbar_init(free0 + 8 * i, 1);     // the publisher's release of the slot
       for (int w = 0; w < 4; w++) s_alive[i][w] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
 
-  if (warp >= C) {
+  if (warp >= C && warp < C + P) {
     // ======================= producer warps =======================
     // Per item (= ring fill): TMA bulk copies of the block's metadata and
     // union records and -- when the tile's feature columns are contiguous
@@ -575,57 +593,86 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     // with gaps left by features that died in the previous layer are
     // gathered with 4-byte cp.async, the staged rows split over the
     // producer warps (named barrier 1 keeps them in step).
+    //
+    // Items are claimed from the layer's atomic counter kMetaAhead + 2
+    // entries ahead (the claim's result is stored one iteration after it was
+    // issued, so it never stalls), and each item's metadata is prefetched
+    // into a shared-memory ring with cp.async, never through registers (a
+    // register copy of a pending load would wait for it): the block
+    // descriptor and the tile's feature columns kMetaAhead items ahead, the
+    // staged-row list (whose address is in the descriptor) two items ahead.
     const int pw = warp - C;
     const int ptid = pw * 32 + lane;
+    // This thread's first gather4 quad: quads are dealt round-robin over the
+    // producer warps (lane-major), because a TMA instruction takes uniform
+    // operands -- a warp issues its lanes' ops one after another, so 34 quads
+    // in one warp would serialise ~34 issue rounds behind the others.
+    const int qd0 = lane * P + pw;
     auto pbar = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(P * 32) : "memory"); };
-    // Item metadata is fetched one item ahead: the next item's index (atomic),
-    // block descriptor, feature columns and first staged-row quad are loaded
-    // while this item's slot is awaited and its copies are issued, so none of
-    // those global round trips sits between a slot turning free and its fill.
-    struct ItemMeta {
-      int item, t, b, v, c4x, c4y, c4z, c4w;
-      int src[FPL];
-    };
-    auto fetch = [&](int item, ItemMeta &im) {
-      im.item = item;
+    char *const mring = smem + A.mring_off;
+    auto ment = [&](int j) { return mring + (j % kMetaRing) * A.mentry_bytes; };
+    // entry layout: int desc[8] | int ain[T] | int fp[fpcap]
+    auto item_of = [&](int j) { return s_items[j & 7]; };
+    auto prefetch_desc = [&](int j) {  // descriptor + feature columns of item j
+      const int item = item_of(j);
       if (item >= items) return;
-      im.t = item / nb;
-      im.b = item - im.t * nb;
-      im.v = lane < 8 ? __ldg(A.L.blocks + (int64_t)im.b * 8 + lane) : 0;
-      const int valid = min(T, M - im.t * T);
-#pragma unroll
-      for (int q = 0; q < FPL; q++) {
-        const int f = 32 * q + lane;
-        im.src[q] = f < valid ? __ldg(A.a_in + im.t * T + f) : -1;
-      }
-      // this thread's first staged-row quad (contiguous path)
-      const int meta_off = __shfl_sync(0xffffffffu, im.v, 4);
-      const int fp_cnt = __shfl_sync(0xffffffffu, im.v, 5);
-      const int32_t *fp = A.L.meta + meta_off;
-      const int qd = ptid;
-      if (4 * qd + 3 < fp_cnt) {
-        const int4 c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
-        im.c4x = c4.x; im.c4y = c4.y; im.c4z = c4.z; im.c4w = c4.w;
-      } else if (4 * qd < fp_cnt) {
-        im.c4x = __ldg(fp + 4 * qd);
-        im.c4y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : im.c4x;
-        im.c4z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : im.c4x;
-        im.c4w = im.c4x;
+      const int t = item / nb, b = item - (item / nb) * nb;
+      const uint32_t e = (uint32_t)__cvta_generic_to_shared(ment(j));
+      if (ptid < 2) {
+        cp_async16(e + 16 * ptid, A.L.blocks + (int64_t)b * 8 + 4 * ptid);
+      } else if (ptid < 2 + T / 4) {
+        const int q = ptid - 2;  // a_in has ld >= (t+1)*T entries; lanes past M are masked
+        cp_async16(e + 32 + 16 * q, A.a_in + t * T + 4 * q);
       }
     };
-    ItemMeta cur;
-    if (ptid == 0) s_pitem[0] = atomicAdd(A.work, 1);
+    auto prefetch_fp = [&](int j) {  // staged-row list of item j (descriptor landed)
+      const int item = item_of(j);
+      if (item >= items) return;
+      const char *en = ment(j);
+      const int meta_off = reinterpret_cast<const int *>(en)[4];
+      const int fp_cnt = reinterpret_cast<const int *>(en)[5];
+      const uint32_t e = (uint32_t)__cvta_generic_to_shared(en) + 32 + 4 * T;
+      for (int q = ptid; 4 * q < fp_cnt; q += P * 32)
+        cp_async16(e + 16 * q, A.L.meta + meta_off + 4 * q);
+    };
+    PROF_DECL
+    int claim = 0;
+    if (ptid == 0) {
+      // entries 0..kMetaAhead in one claim (a CTA's items must be increasing:
+      // the first one past the end stops the producer), then one per entry
+      const int base = atomicAdd(A.work, kMetaAhead + 1);
+      for (int j = 0; j <= kMetaAhead; j++) s_items[j] = base + j;
+      claim = atomicAdd(A.work, 1);  // entry kMetaAhead + 1
+    }
     pbar();
-    fetch(s_pitem[0], cur);
+    for (int j = 0; j < kMetaAhead; j++) {
+      prefetch_desc(j);
+      cp_async_commit();
+    }
+    cp_async_wait<0>();
+    pbar();
+    prefetch_fp(0);
+    prefetch_fp(1);
+    cp_async_commit();
+    cp_async_wait<0>();
     for (int k = 0;; k++) {
-      const int item = cur.item;
+      // item k: descriptor (group k - kMetaAhead) and staged rows (group k - 2)
+      // have landed once at most one group (the newest) is pending
+      if (ptid == 0) {
+        s_items[(k + kMetaAhead + 1) & 7] = claim;  // claimed one iteration ago
+        claim = atomicAdd(A.work, 1);                // entry k + kMetaAhead + 2
+      }
+      cp_async_wait<1>();
+      pbar();
+      const int item = item_of(k);
       if (item >= items) {
+        cp_async_wait<0>();
         if (pw == 0) {
           // end markers in the next nbuf entries; a consumer warp waits at most
           // ceil(C / gpi) <= nbuf entries past the last one it served
           for (int e = 0; e < nbuf; e++, k++) {
             const int slot = k % nbuf;
-            mbar_wait(empty0 + 8 * slot, ((uint32_t)(k / nbuf) & 1u) ^ 1u);
+            mbar_wait(free0 + 8 * slot, ((uint32_t)(k / nbuf) & 1u) ^ 1u);
             if (lane == 0) {
               Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
               h->item = -1;
@@ -637,27 +684,35 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         }
         break;
       }
-      int nxt = 0;
-      if (ptid == 0) nxt = atomicAdd(A.work, 1);  // consumed after this item's copies
-      const int t = cur.t, b = cur.b, v = cur.v;
-      const int ng = __shfl_sync(0xffffffffu, v, 1);
-      const int nst = __shfl_sync(0xffffffffu, v, 2);
-      const int meta_off = __shfl_sync(0xffffffffu, v, 4);
-      const int fp_cnt = __shfl_sync(0xffffffffu, v, 5);
-      const int rec_off = __shfl_sync(0xffffffffu, v, 6);
-      const int rec_cnt = __shfl_sync(0xffffffffu, v, 7);
-      // feature columns 32q + lane (q < FPL) of tile t: gathers then write 32
-      // consecutive smem words per instruction (bank-conflict free)
-      const int p0 = __shfl_sync(0xffffffffu, cur.src[0], 0);
+      const int *en = reinterpret_cast<const int *>(ment(k));
+      const int t = item / nb, b = item - (item / nb) * nb;
+      const int ng = en[1], nst = en[2], meta_off = en[4], fp_cnt = en[5];
+      const int rec_off = en[6], rec_cnt = en[7];
+      const int *ain = en + 8;
+      const int *sfp = en + 8 + T;
+      // feature columns 32q + lane (q < FPL) of tile t
+      const int valid = min(T, M - t * T);
+      int src[FPL];
+#pragma unroll
+      for (int q = 0; q < FPL; q++) src[q] = 32 * q + lane < valid ? ain[32 * q + lane] : -1;
+      const int p0 = ain[0];
       bool mine_contig = true;
 #pragma unroll
-      for (int q = 0; q < FPL; q++)
-        mine_contig &= cur.src[q] < 0 || cur.src[q] == p0 + 32 * q + lane;
+      for (int q = 0; q < FPL; q++) mine_contig &= src[q] < 0 || src[q] == p0 + 32 * q + lane;
       const bool contig = __all_sync(0xffffffffu, mine_contig) && (p0 & 3) == 0;
+      int4 c4 = make_int4(0, 0, 0, 0);
+      if (4 * qd0 < fp_cnt) {
+        c4 = *reinterpret_cast<const int4 *>(sfp + 4 * qd0);
+        if (4 * qd0 + 1 >= fp_cnt) c4.y = c4.x;
+        if (4 * qd0 + 2 >= fp_cnt) c4.z = c4.x;
+        if (4 * qd0 + 3 >= fp_cnt) c4.w = c4.x;
+      }
+      PROF_MARK(3);  // [3] metadata from the prefetch ring
 
       const int slot = k % nbuf;
       const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
-      if (pw == 0) mbar_wait(empty0 + 8 * slot, phase ^ 1u);  // others park at the bar.sync below
+      if (pw == 0) mbar_wait(free0 + 8 * slot, phase ^ 1u);  // others park at the bar.sync below
+      PROF_MARK(0);  // [0] waiting for an empty slot
       const uint32_t full = full0 + 8 * slot;
       const uint32_t buf = sbase + slot * A.buf_bytes;
       const uint32_t smeta = buf + kHeaderBytes;
@@ -667,51 +722,59 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
       const int quads = (fp_cnt + 3) >> 2;
       if (ptid == 0) {
+#ifdef SPDNN_ABLATE_STAGE
+        const uint32_t tx = (uint32_t)meta_words * 4u + rec_b;
+#else
         const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
                             (contig ? (uint32_t)quads * 4u * G::kRow : 0u);
+#endif
         mbar_expect_tx(full, tx);
       }
       pbar();  // expected bytes registered before any copy can complete
+      PROF_MARK(1);  // [1] barrier A (slot free, expected bytes set)
       if (ptid == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
-      if (ptid == 1 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
-      const int32_t *fp = A.L.meta + meta_off;
+      if (ptid == 32 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
+      PROF_MARK(2);  // [2] bulk copies of meta + records
+#ifdef SPDNN_ABLATE_STAGE
+      if (contig) {  // diagnostics: staged rows are not copied (not expected either)
+      } else
+#endif
       if (contig) {
-        if (ptid < quads)
-          tma_gather4(sy + (uint32_t)ptid * 4u * G::kRow, &A.tmap_in, p0, cur.c4x, cur.c4y,
-                      cur.c4z, cur.c4w, full);
-        for (int qd = ptid + P * 32; qd < quads; qd += P * 32) {  // footprints > 512 rows
-          int4 c4;
-          if (4 * qd + 3 < fp_cnt) {
-            c4 = __ldg(reinterpret_cast<const int4 *>(fp) + qd);
-          } else {
-            c4.x = __ldg(fp + 4 * qd);
-            c4.y = 4 * qd + 1 < fp_cnt ? __ldg(fp + 4 * qd + 1) : c4.x;
-            c4.z = 4 * qd + 2 < fp_cnt ? __ldg(fp + 4 * qd + 2) : c4.x;
-            c4.w = c4.x;
-          }
-          tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c4.x, c4.y, c4.z, c4.w,
+        if (qd0 < quads)
+          tma_gather4(sy + (uint32_t)qd0 * 4u * G::kRow, &A.tmap_in, p0, c4.x, c4.y, c4.z, c4.w,
                       full);
+        for (int qd = P * 32 + ptid; qd < quads; qd += P * 32) {  // footprints > 512 rows
+          int4 c = *reinterpret_cast<const int4 *>(sfp + 4 * qd);
+          if (4 * qd + 1 >= fp_cnt) c.y = c.x;
+          if (4 * qd + 2 >= fp_cnt) c.z = c.x;
+          if (4 * qd + 3 >= fp_cnt) c.w = c.x;
+          tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c.x, c.y, c.z, c.w, full);
         }
+        PROF_MARK(6);  // [6] TMA gather4 issue (contiguous tiles)
       } else {
         // staged rows s = 32 pw .. : the warp's 32 lanes copy the row's T features
         for (int s0 = pw * 32; s0 < fp_cnt; s0 += P * 32) {
-          const int my = s0 + lane < fp_cnt ? __ldg(fp + s0 + lane) : 0;
+          const int my = s0 + lane < fp_cnt ? sfp[s0 + lane] : 0;
           const int cnt = min(32, fp_cnt - s0);
           for (int i = 0; i < cnt; i++) {
             const int64_t c = __shfl_sync(0xffffffffu, my, i);
             const float *row = A.y_in + c * A.ld;
             const uint32_t dst = sy + (uint32_t)(s0 + i) * G::kRow + 4 * lane;
 #pragma unroll
-            for (int q = 0; q < FPL; q++)
-              cp_async4(dst + 128 * q, row + max(cur.src[q], 0), cur.src[q] >= 0);
+            for (int q = 0; q < FPL; q++) cp_async4(dst + 128 * q, row + max(src[q], 0), src[q] >= 0);
           }
         }
         mbar_cp_async_arrive_inc(full);
+        PROF_MARK(7);  // [7] 4-byte cp.async gathers (tiles with gaps)
       }
-      // s_pitem is double-buffered: entry (k+1)&1 was last read before this
-      // iteration's first barrier
-      if (ptid == 0) s_pitem[(k + 1) & 1] = nxt;
-      pbar();  // every producer's copies issued and counted; next item index visible
+      // metadata for items k + kMetaAhead (descriptor) and k + 2 (staged rows;
+      // its descriptor landed with this iteration's wait): ring entry k's
+      // slot is reused by k + kMetaRing >= k + kMetaAhead + 1 only
+      prefetch_desc(k + kMetaAhead);
+      prefetch_fp(k + 2);
+      cp_async_commit();
+      pbar();  // every producer's copies issued and counted
+      PROF_MARK(4);  // [4] barrier B
       if (ptid == 0) {
         Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
         h->item = item;
@@ -724,7 +787,75 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         h->fp_cnt = fp_cnt;
         mbar_arrive(full);
       }
-      fetch(s_pitem[(k + 1) & 1], cur);
+      PROF_MARK(5);  // [5] header
+    }
+    PROF_FLUSH(8)
+    return;
+  }
+
+  if (warp == C + P) {
+    // ======================= publisher warp =======================
+    // Once every unit of ring entry k has arrived on empty[slot], read and
+    // clear the entry's activity bits, release the slot to the producer
+    // (free[slot]) and only then do the global part off the fill path: OR
+    // the bits into the tile's word, count the tile's finished blocks, and
+    // the item that completes tile t appends the tile's survivors to
+    // a_out / cat_out (pruning without a pass over Y).
+    for (int k = 0;; k++) {
+      const int slot = k % nbuf;
+      const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
+      mbar_wait(full0 + 8 * slot, phase);
+      const int item = reinterpret_cast<const volatile Header *>(smem + slot * A.buf_bytes)->item;
+      const int t = reinterpret_cast<const volatile Header *>(smem + slot * A.buf_bytes)->t;
+      if (item < 0) break;
+      mbar_wait(empty0 + 8 * slot, phase);
+      uint32_t wv = lane < FPL ? s_alive[slot][lane] : 0u;
+      if (lane < FPL) s_alive[slot][lane] = 0u;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(free0 + 8 * slot);
+      if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * t + lane], wv);
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        // release our activity bits before the count; the last arrival
+        // acquires everyone's (acq_rel instead of a full __threadfence)
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n"
+                     : "=r"(old)
+                     : "l"(A.tile_done + t)
+                     : "memory");
+        last = old == nb - 1;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        if (lane < FPL) {
+          wv = atomicOr(&A.tile_alive[FPL * t + lane], 0u);
+          A.tile_alive[FPL * t + lane] = 0u;
+        }
+        if (lane == 0) A.tile_done[t] = 0;
+        uint32_t mw[FPL];
+        int tot = 0, below = 0;
+#pragma unroll
+        for (int q = 0; q < FPL; q++) {
+          mw[q] = __shfl_sync(0xffffffffu, wv, q);
+          tot += __popc(mw[q]);
+          below += __popc(mw[q] & ((1u << lane) - 1u));  // alive features of lanes < this
+        }
+        int base = 0;
+        if (lane == 0 && tot) base = atomicAdd(A.m_out, tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        // this lane's features FPL*lane + q, in feature order
+        int rank = base + below;
+#pragma unroll
+        for (int q = 0; q < FPL; q++) {
+          if ((mw[q] >> lane) & 1u) {
+            const int j = t * T + FPL * lane + q;
+            A.a_out[rank] = j;
+            A.cat_out[rank] = A.cat_in[j];
+            rank++;
+          }
+        }
+      }
     }
     return;
   }
@@ -744,6 +875,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   int k = warp / gpi, g = warp - (warp / gpi) * gpi;
   int slot = k % nbuf;
   uint32_t phase = (uint32_t)(k / nbuf) & 1u;
+  PROF_DECL
   for (;; ) {
     const char *buf = smem + slot * A.buf_bytes;
     const volatile Header *vh = reinterpret_cast<const volatile Header *>(buf);
@@ -758,6 +890,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       mbar_wait(full0 + 8 * slot, phase);  // the phase of entry k itself
     }
     const Header h = *reinterpret_cast<const Header *>(buf);
+    PROF_MARK(0);  // [0] waiting for data
     if (h.item < 0) break;
     if (g < h.ng) {
       const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
@@ -767,7 +900,11 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       u64 acc[H * R];
 #pragma unroll
       for (int r = 0; r < H * R; r++) acc[r] = 0ull;
+#ifdef SPDNN_ABLATE_COMPUTE
+      if (false) {  // diagnostics: no record loop
+#else
       if (MASK) {
+#endif
         accumulate_mask<R, FMA, FPL>(acc, recs + meta[seg_base + 2 * g],
                                      meta[seg_base + 2 * g + 1],
                                      (uint32_t)__cvta_generic_to_shared(ybase), w_mask, negz2);
@@ -776,6 +913,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
                                    meta[seg_base + 2 * g + 1], ybase, negz2);
       }
       if (h.nst > 1) accumulate_global<R, FMA, FPL, MASK>(A, acc, h.b, h.t, lane, M, negz2);
+      PROF_MARK(1);  // [1] record loop
       // output rows and their biases (staged with the block metadata) are read
       // only now, so they hold no registers across the record loop
       asm volatile("" ::: "memory");
@@ -789,65 +927,12 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         bias[r] = mbias[r];
       }
       epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
+      PROF_MARK(2);  // [2] epilogue
     }
+    // the unit's activity bits went to s_alive[slot] (lane 0's shared
+    // atomics, ordered before its arrival by the mbarrier's release); the
+    // publisher warp folds them into the tile once every unit has arrived
     __syncwarp();
-    int bookkeeper = 0;
-    if (lane == 0) {
-      __threadfence_block();
-      bookkeeper = atomicAdd(&s_done[slot], 1) == gpi - 1;
-    }
-    bookkeeper = __shfl_sync(0xffffffffu, bookkeeper, 0);
-    if (bookkeeper) {
-      // every unit of the item has published its activity bits
-      __threadfence_block();
-      uint32_t wv = lane < FPL ? s_alive[slot][lane] : 0u;
-      __syncwarp();
-      if (lane < FPL) s_alive[slot][lane] = 0u;
-      if (lane == 0) s_done[slot] = 0;
-      int last = 0;
-      if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * h.t + lane], wv);
-      __syncwarp();
-      if (lane == 0) {
-        // release our activity bits before the count; the last arrival
-        // acquires everyone's (acq_rel instead of a full __threadfence)
-        int old;
-        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n"
-                     : "=r"(old)
-                     : "l"(A.tile_done + h.t)
-                     : "memory");
-        last = old == nb - 1;
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        if (lane < FPL) {
-          wv = atomicOr(&A.tile_alive[FPL * h.t + lane], 0u);
-          A.tile_alive[FPL * h.t + lane] = 0u;
-        }
-        if (lane == 0) A.tile_done[h.t] = 0;
-        uint32_t mw[FPL];
-        int tot = 0, below = 0;
-#pragma unroll
-        for (int q = 0; q < FPL; q++) {
-          mw[q] = __shfl_sync(0xffffffffu, wv, q);
-          tot += __popc(mw[q]);
-          below += __popc(mw[q] & ((1u << lane) - 1u));  // alive features of lanes < this
-        }
-        int base = 0;
-        if (lane == 0 && tot) base = atomicAdd(A.m_out, tot);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        // this lane's features FPL*lane + q, in feature order
-        int rank = base + below;
-#pragma unroll
-        for (int q = 0; q < FPL; q++) {
-          if ((mw[q] >> lane) & 1u) {
-            const int j = h.t * T + FPL * lane + q;
-            A.a_out[rank] = j;
-            A.cat_out[rank] = A.cat_in[j];
-            rank++;
-          }
-        }
-      }
-    }
     if (lane == 0) mbar_arrive(empty0 + 8 * slot);
     g += C;
     while (g >= gpi) {
@@ -858,7 +943,9 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         phase ^= 1u;
       }
     }
+    PROF_MARK(3);  // [3] unit bookkeeping, tile publishing
   }
+  PROF_FLUSH(0)
 }
 
 // ---- launch configuration ---------------------------------------------------
@@ -916,13 +1003,19 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   const size_t rec = up128((size_t)L.max_records_per_stage * L.record_words * 4 + 16);
   const size_t ys = (size_t)((L.max_fp_per_stage + 3) & ~3) * G::kRow;  // gather4: rows in 4s
   const size_t buf = (kHeaderBytes + meta + rec + ys + 127) / 128 * 128;
-  const size_t budget = optin - 2048;  // static shared memory + reserve
+  // producer metadata ring: descriptor | feature columns | staged-row list
+  const size_t fpcap = (size_t)((L.max_fp_per_stage + 3) & ~3);
+  const size_t mentry = ((8 + G::kTileF + fpcap) * 4 + 15) / 16 * 16;
+  const size_t mring = (size_t)kMetaRing * mentry;
+  const size_t budget = optin - 2048 - mring;  // static shared memory + reserve
   const int nbuf = (int)std::min<size_t>(kMaxBufs, budget / buf);
   if (nbuf < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
   // units per item: at least the block's groups, and enough that a consumer
   // warp's consecutive units are at most nbuf ring entries apart
   const int gpi = std::max(std::max(1, L.max_groups_per_block), (G::kC + nbuf - 1) / nbuf);
-  const size_t smem = (size_t)nbuf * buf;
+  const size_t smem = (size_t)nbuf * buf + mring;
+  A.mring_off = (uint32_t)(nbuf * buf);
+  A.mentry_bytes = (uint32_t)mentry;
   A.meta_bytes = (uint32_t)meta;
   A.rec_bytes = (uint32_t)rec;
   A.buf_bytes = (uint32_t)buf;
@@ -1141,6 +1234,20 @@ extern "C" int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int
   gather_out_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(y, n, ld, a, perm, m, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SPDNN_OK : spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
+}
+
+extern "C" int spdnn_profile_read(uint64_t *out, int32_t n, int32_t reset) {
+  if (!out || n < 0 || n > 16) return spdnn_fail(SPDNN_EINVAL, "spdnn_profile_read: bad args");
+  unsigned long long h[16];
+  cudaError_t e = cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
+  if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
+  for (int i = 0; i < n; i++) out[i] = h[i];
+  if (reset) {
+    std::memset(h, 0, sizeof(h));
+    e = cudaMemcpyToSymbol(g_prof, h, sizeof(h));
+    if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
+  }
+  return SPDNN_OK;
 }
 
 extern "C" int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_sm,
