@@ -412,6 +412,7 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
                                                 const float *bias, int j0, int valid,
                                                 bool &tiny) {
   constexpr int H = FPL / 2;
+  const char *obase = reinterpret_cast<const char *>(A.y_out) + 4ull * (uint32_t)j0;
   // FMA form (finite values guaranteed, else the run is redone): per feature the
   // running unsigned min of bits(v) - 1 gives both tests: v > 0 exists <=> the
   // min is not 0xffffffff, and a v in (0, tiny) exists <=> min < bits(tiny) - 1.
@@ -451,7 +452,9 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
 #ifdef SPDNN_ABLATE_STORE
     if (rows[k] >= 0) continue;  // diagnostics: no output stores
 #endif
-    float *dst = A.y_out + (int64_t)rows[k] * A.ld + j0;
+    // one IMAD.WIDE.U32 per row: row * (ld * 4) + (y_out + 4 * j0); ld * 4 < 2^32
+    float *dst = (float *)(
+        obase + (unsigned long long)(uint32_t)rows[k] * (uint32_t)(A.ld * 4));
     if (FULL) {
       if (FPL == 4) *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
       else *reinterpret_cast<float2 *>(dst) = make_float2(x[0], x[1]);
