@@ -626,6 +626,10 @@ def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
         raise ModelError("inputs do not match model width")
     edges = inputs.total_inputs * (edges_per_input if edges_per_input is not None
                                    else sum(getattr(net, "nnz", [])))
+    if not values and net.num_layers and m >= 4 * PIPELINE_MIN_FEATURES:
+        res = _infer_pipelined(net, inputs, edges)
+        if res is not None:
+            return res
     if net.num_layers == 0 or m == 0:
         return _trivial_result(net.num_layers, inputs, edges // max(inputs.total_inputs, 1))
     ws = workspace(n, m, net.num_layers)
@@ -667,6 +671,115 @@ def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
     return InferenceResult(final=final, categories=cats_np.copy(),
                            per_layer=_outcomes(counts, net), elapsed_seconds=elapsed,
                            edges_processed=edges, device_seconds=device)
+
+
+PIPELINE_MIN_FEATURES = 4096  # smallest first chunk of the upload/compute pipeline
+PIPELINE_HEAD = 8             # the first chunk is 1/8 of the batch
+_pipe_cache: dict = {}
+
+
+class _PipeBuffers:
+    """Device buffers of the chunked upload/compute pipeline: two raw-upload
+    buffers (chunk c+1 lands while chunk c computes), the shared neuron-major
+    feature buffers, and per chunk the index/category/count arrays that hold
+    its survivors until the single read at the end."""
+
+    def __init__(self, n: int, cap: int, chunks: int, num_layers: int, device):
+        torch = _torch()
+        self.key = (n, cap, chunks, num_layers)
+        self.ws = Workspace(n, cap, num_layers, device)  # y[0..1], scratch, iota
+        self.x = [self.ws.x, torch.empty((cap, n), dtype=torch.float32, device=device)]
+        i32, i64 = torch.int32, torch.int64
+        self.a = [[torch.empty(self.ws.ld, dtype=i32, device=device) for _ in range(2)]
+                  for _ in range(chunks)]
+        self.cat = [[torch.empty(self.ws.ld, dtype=i64, device=device) for _ in range(2)]
+                    for _ in range(chunks)]
+        self.counts = torch.zeros((chunks, num_layers + 1), dtype=i32, device=device)
+        self.guard = torch.zeros(chunks, dtype=i32, device=device)
+        self.up = torch.cuda.Stream(device=device)
+
+
+def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
+    """values=False inference with the input upload overlapped: the batch is
+    cut into two feature ranges (features never interact, so each runs the
+    whole network on its own): a head of 1/PIPELINE_HEAD of the batch, whose
+    upload is the only one exposed, and the rest, copied host->device on a
+    side stream while the head's layers run (the head computes for about as
+    long as the rest takes to upload, and only one extra launch per layer is
+    paid). One host synchronisation at the end reads every chunk's counts.
+    Returns None when an arithmetic guard fired (the caller then takes the
+    unchunked path, which reruns in the exact form)."""
+    torch = _torch()
+    n, m, L = net.neurons, inputs.active_count, net.num_layers
+    head = max(PIPELINE_MIN_FEATURES, m // PIPELINE_HEAD)
+    bounds = [(0, head), (head, m)]
+    chunks = 2
+    cap = max(hi - lo for lo, hi in bounds)
+    dev = torch.cuda.current_device()
+    key = (dev, threading.get_ident())
+    with _cache_lock:
+        pb = _pipe_cache.get(key)
+        if pb is None or pb.key != (n, cap, chunks, L):
+            _pipe_cache.pop(key, None)
+            _ws_cache.pop(key, None)
+            torch.cuda.empty_cache()
+            pb = _PipeBuffers(n, cap, chunks, L, torch.device("cuda", dev))
+            _pipe_cache[key] = pb
+    ws = pb.ws
+    host = torch.from_numpy(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
+    cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
+    main, up = torch.cuda.current_stream(), pb.up
+    lib = _native.lib()
+    opts = run_opts(net)
+    freed = [None, None]
+    pb.guard.zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(main)
+    for c, (lo, hi) in enumerate(bounds):
+        mc, xb = hi - lo, pb.x[c % 2]
+        with torch.cuda.stream(up):
+            if freed[c % 2] is not None:
+                up.wait_event(freed[c % 2])  # chunk c-2 has been laid out
+            xb[:mc].copy_(host[lo:hi], non_blocking=True)
+            pb.cat[c][0][:mc].copy_(cats[lo:hi], non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(up)
+        main.wait_event(ready)
+        guard = ctypes.c_void_p(pb.guard.data_ptr() + 4 * c)
+        _native.check(lib.spdnn_transpose_in(
+            _dptr(xb), n, mc, _dptr(ws.y[0]), ws.ld, guard, net.tiny, net.huge,
+            _stream_ptr(torch)), "spdnn_transpose_in")
+        freed[c % 2] = torch.cuda.Event()
+        freed[c % 2].record(main)
+        for t in (xb, pb.cat[c][0]):
+            t.record_stream(main)
+        pb.a[c][0][:mc].copy_(ws.iota[:mc])
+        cnt = pb.counts[c]
+        cnt.zero_()
+        cnt[0] = mc
+        ws.work.zero_()
+        sc = _native.Scratch(ws.tile_done.data_ptr(), ws.tile_alive.data_ptr(),
+                             ws.work.data_ptr(), pb.guard.data_ptr() + 4 * c)
+        _native.check(lib.spdnn_infer_layers(
+            L, net.layer_devs, _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
+            _dptr(pb.a[c][0]), _dptr(pb.a[c][1]), _dptr(pb.cat[c][0]), _dptr(pb.cat[c][1]),
+            _dptr(cnt), ctypes.byref(sc), ctypes.byref(opts), _stream_ptr(torch)),
+            "spdnn_infer_layers")
+    ev1.record(main)
+    host_counts = torch.cat([pb.counts.reshape(-1).to(torch.int64),
+                             pb.guard.to(torch.int64)]).cpu().numpy()
+    elapsed = time.perf_counter() - t0
+    counts = host_counts[:-chunks].reshape(chunks, L + 1)
+    if int(np.bitwise_or.reduce(host_counts[-chunks:])) & (2 | (1 if opts.fma_form else 0)):
+        return None
+    surv = counts[:, L]
+    cat_parts = [pb.cat[c][L % 2][: int(surv[c])] for c in range(chunks)]
+    cats_np = torch.sort(torch.cat(cat_parts))[0].cpu().numpy().astype(np.int64)
+    return InferenceResult(final=None, categories=cats_np, per_layer=_outcomes(counts.sum(0), net),
+                           elapsed_seconds=elapsed, edges_processed=edges,
+                           device_seconds=ev0.elapsed_time(ev1) / 1e3)
 
 
 class WeightStreamer:

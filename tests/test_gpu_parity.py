@@ -359,3 +359,31 @@ def test_chunked_device_network_infer_device(cuda_ok):
     assert same_bits(got.final.data, want.final.data)
     assert [(o.active_before, o.active_after) for o in got.per_layer] == \
         [(o.active_before, o.active_after) for o in want.per_layer]
+
+
+def test_pipelined_upload_matches_single_pass(cuda_ok):
+    """values=False on a large host batch takes the chunked upload/compute
+    pipeline (engine._infer_pipelined): same categories and per-layer counts as
+    the one-pass run and the oracle's; a NaN input makes it fall back to the
+    guarded path with the same answer."""
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=40, connections_per_neuron=32, bias_value=-0.3, seed=3))
+    inputs = ingest.generate_synthetic_inputs(1024, 5 * engine.PIPELINE_MIN_FEATURES + 77, 0.3,
+                                              seed=5)
+    full = engine.infer(model, inputs, InferenceConfig())
+    piped = engine.infer(model, inputs, InferenceConfig(), values=False)
+    assert piped.final is None
+    assert np.array_equal(piped.categories, full.categories)
+    assert [(o.active_before, o.active_after) for o in piped.per_layer] == \
+        [(o.active_before, o.active_after) for o in full.per_layer]
+    pick = np.arange(0, inputs.active_count, 97)
+    sub = make_feature_batch(1024, np.asfortranarray(inputs.data[:, pick]), categories=pick,
+                             total_inputs=inputs.total_inputs)
+    ref = oracle.infer(model, sub, threads=4, want_final=False)
+    assert np.intersect1d(piped.categories, pick).tolist() == ref.categories.tolist()
+    data = np.asarray(inputs.data).copy()
+    data[3, 9000] = np.nan
+    poisoned = make_feature_batch(1024, data)
+    a = engine.infer(model, poisoned, InferenceConfig(), values=False)
+    b = engine.infer(model, poisoned, InferenceConfig())
+    assert np.array_equal(a.categories, b.categories)
