@@ -50,8 +50,12 @@
 namespace {
 
 constexpr int kMaxBufs = 4;
-constexpr int kMetaAhead = 4;  // producer metadata prefetch distance (items)
-constexpr int kMetaRing = 6;   // metadata ring entries (> kMetaAhead)
+constexpr int kMetaAhead = 5;  // producer: block descriptors prefetched this many items ahead
+constexpr int kFpAhead = 3;    // producer: staged-row lists prefetched this many items ahead
+constexpr int kMetaRing = 7;   // metadata ring entries (> kMetaAhead)
+#ifndef SPDNN_L2_PREFETCH
+#define SPDNN_L2_PREFETCH 0    // L2 prefetch of the next item's staged rows (gather4): measured slower
+#endif
 #ifndef SPDNN_MASK_CONSUMERS
 #define SPDNN_MASK_CONSUMERS 20
 #endif
@@ -144,6 +148,14 @@ __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap *tm
       " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(sdst),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
       "r"(bar)
+      : "memory");
+}
+// TMA gather4 into L2 only (no shared-memory destination, no completion)
+__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap *tmap, int col, int r0,
+                                                     int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n"
+      ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
 }
 // TMA bulk copy global -> this CTA's shared memory, completion as tx bytes
@@ -350,9 +362,24 @@ __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int c
 // exactly the reference's sum, which never visits those columns. Each
 // group's run is padded to a multiple of 4 with zero words (no-ops).
 template <int R, bool FMA, int FPL>
+__device__ __forceinline__ void mask_record(u64 *acc, uint32_t wd, const YVec<FPL> &y, float w,
+                                            u64 negz2) {
+  constexpr int H = FPL / 2;
+#pragma unroll
+  for (int k = 0; k < R; k++) {
+    if (wd & (1u << k)) {
+#pragma unroll
+      for (int h = 0; h < H; h++) {
+        if (FMA) fma2_acc(acc[H * k + h], y.v[h], w);
+        else mul_add2_acc(acc[H * k + h], y.v[h], w, negz2);
+      }
+    }
+  }
+}
+
+template <int R, bool FMA, int FPL>
 __device__ __forceinline__ void accumulate_mask(u64 *acc, const uint32_t *recs, int cnt,
                                                 uint32_t ybase, float w, u64 negz2) {
-  constexpr int H = FPL / 2;
   const uint4 *rp = reinterpret_cast<const uint4 *>(recs);
   const uint4 *const end = rp + (cnt >> 2);
 #pragma unroll kMaskUnroll
@@ -363,18 +390,7 @@ __device__ __forceinline__ void accumulate_mask(u64 *acc, const uint32_t *recs, 
 #pragma unroll
     for (int j = 0; j < 4; j++) y[j].load_s(ybase + (wd[j] >> (15 + Geo<FPL>::kOffShift)));
 #pragma unroll
-    for (int j = 0; j < 4; j++) {
-#pragma unroll
-      for (int k = 0; k < R; k++) {
-        if (wd[j] & (1u << k)) {
-#pragma unroll
-          for (int h = 0; h < H; h++) {
-            if (FMA) fma2_acc(acc[H * k + h], y[j].v[h], w);
-            else mul_add2_acc(acc[H * k + h], y[j].v[h], w, negz2);
-          }
-        }
-      }
-    }
+    for (int j = 0; j < 4; j++) mask_record<R, FMA, FPL>(acc, wd[j], y[j], w, negz2);
   }
 }
 
@@ -654,13 +670,14 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     }
     cp_async_wait<0>();
     pbar();
-    prefetch_fp(0);
-    prefetch_fp(1);
+    for (int j = 0; j < kFpAhead; j++) prefetch_fp(j);
     cp_async_commit();
     cp_async_wait<0>();
     for (int k = 0;; k++) {
-      // item k: descriptor (group k - kMetaAhead) and staged rows (group k - 2)
-      // have landed once at most one group (the newest) is pending
+      // item k: descriptor (group k - kMetaAhead) and staged rows (group
+      // k - kFpAhead) have landed once at most one group (the newest) is
+      // pending; so have item k+1's (L2 prefetch) and item k+kFpAhead's
+      // descriptor (group k - 2)
       if (ptid == 0) {
         s_items[(k + kMetaAhead + 1) & 7] = claim;  // claimed one iteration ago
         claim = atomicAdd(A.work, 1);                // entry k + kMetaAhead + 2
@@ -770,11 +787,37 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         mbar_cp_async_arrive_inc(full);
         PROF_MARK(7);  // [7] 4-byte cp.async gathers (tiles with gaps)
       }
-      // metadata for items k + kMetaAhead (descriptor) and k + 2 (staged rows;
-      // its descriptor landed with this iteration's wait): ring entry k's
-      // slot is reused by k + kMetaRing >= k + kMetaAhead + 1 only
+#if SPDNN_L2_PREFETCH
+      {
+        // the next item's staged rows into L2: its fill, one slot turnover
+        // from now, then reads L2 instead of DRAM
+        const int nitem = item_of(k + 1);
+        if (nitem < items) {
+          const int *en1 = reinterpret_cast<const int *>(ment(k + 1));
+          const int t1 = nitem / nb;
+          const int fp1 = en1[5];
+          const int v1 = min(T, M - t1 * T);
+          const int q0 = en1[8];
+          bool mc = true;
+#pragma unroll
+          for (int q = 0; q < FPL; q++)
+            mc &= 32 * q + lane >= v1 || en1[8 + 32 * q + lane] == q0 + 32 * q + lane;
+          if (__all_sync(0xffffffffu, mc) && (q0 & 3) == 0 && 4 * qd0 < fp1) {
+            const int *f1 = en1 + 8 + T + 4 * qd0;
+            const int x0 = f1[0];
+            const int x1 = 4 * qd0 + 1 < fp1 ? f1[1] : x0;
+            const int x2 = 4 * qd0 + 2 < fp1 ? f1[2] : x0;
+            const int x3 = 4 * qd0 + 3 < fp1 ? f1[3] : x0;
+            tma_prefetch_gather4(&A.tmap_in, q0, x0, x1, x2, x3);
+          }
+        }
+      }
+#endif
+      // metadata for items k + kMetaAhead (descriptor) and k + kFpAhead
+      // (staged rows; its descriptor landed with this iteration's wait):
+      // ring entry k's slot is reused by k + kMetaRing > k + kMetaAhead only
       prefetch_desc(k + kMetaAhead);
-      prefetch_fp(k + 2);
+      prefetch_fp(k + kFpAhead);
       cp_async_commit();
       pbar();  // every producer's copies issued and counted
       PROF_MARK(4);  // [4] barrier B

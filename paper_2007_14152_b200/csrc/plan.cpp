@@ -237,6 +237,7 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
     const int32_t hi_col = c_hi > c_lo ? fp_block[c_hi - 1] : -1;
     for (int64_t i = c_lo; i < c_hi; i++) slot_of[fp_block[i]] = (int32_t)(i - c_lo);
     const int64_t rec_off = (int64_t)pl->records.size() / RW;
+    int64_t real = 0;  // records excluding padding words
     for (size_t gg = g0; gg < g0 + ng; gg++) {
       const int64_t start = (int64_t)pl->records.size() / RW - rec_off;
       int64_t cnt = 0;
@@ -259,7 +260,10 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
         cnt++;
       }
       // mask records: each group's run padded to a multiple of 4 (the kernel
-      // reads 4 records per 16-byte load); padding words are mask 0 (no-op)
+      // reads 4 records per 16-byte load); the padding words are mask 0, so
+      // their FFMA2s are all predicated off (measured cheaper than a tail
+      // loop over the exact count)
+      real += cnt;
       if (pl->uniform)
         while (cnt % 4) {
           pl->records.push_back(0u);
@@ -271,7 +275,7 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
       }
     }
     const int64_t rec_cnt = (int64_t)pl->records.size() / RW - rec_off;
-    pl->union_records += rec_cnt;
+    pl->union_records += real;
     // keep every stage's records 16-byte aligned for the bulk copy (R = 1
     // records are 8 bytes): pad with an unreferenced zero record
     while ((pl->records.size() * 4) % 16) pl->records.push_back(0u);

@@ -75,7 +75,7 @@ class PlanParams:
     rows_per_group: int = 0      # 0 = cost model picks 1, 3 or 7 per layer
     footprint_cap: int = 176     # staged input neurons per block stage (x512 B smem)
     max_groups: int = 20         # row groups per block (one per consumer warp)
-    record_cap: int = 640        # union records per block stage
+    record_cap: int = 800        # union records per block stage
     reorder: bool = True
     uniform_records: bool = True  # one-word mask records when all weights are equal
 

@@ -83,7 +83,8 @@ def test_dense_rows_force_multi_stage():
     plan = _check(layer, PlanParams(rows_per_group=3), rng, m=5)
     extra = plan.stages.reshape(-1, 4)
     assert len(extra) > 0  # some block has several stages
-    assert extra[:, 1].max() <= 160 and plan.max_fp_per_stage <= 160
+    cap = PlanParams().footprint_cap
+    assert extra[:, 1].max() <= cap and plan.max_fp_per_stage <= cap
 
 
 def test_sliding_window_layers_group_well():
