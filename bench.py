@@ -558,6 +558,10 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream()
     opts = engine.run_opts(net)
 
+    import ctypes
+    lib = _native.lib()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+
     def step(evs=None):
         engine.stage_inputs(ws, x_dev, cats_dev, net)
         if evs is None:
@@ -565,21 +569,15 @@ def run_ours(args, cfg):
         ws.counts.zero_()
         ws.counts[0] = m
         ws.work.zero_()
-        import ctypes
-        lib = _native.lib()
-        sp = ctypes.c_void_p(stream.cuda_stream)
-        for l in range(L):
-            i, o = l & 1, (l & 1) ^ 1
-            evs[l].record()
-            _native.check(lib.spdnn_layer_forward(
-                ctypes.byref(net.layer_devs[l]), engine._dptr(net.bias), engine._dptr(ws.y[i]),
-                engine._dptr(ws.y[o]), ws.ld, engine._dptr(ws.a[i]), engine._dptr(ws.cat[i]),
-                ctypes.c_void_p(ws.counts.data_ptr() + 4 * l), engine._dptr(ws.a[o]),
-                engine._dptr(ws.cat[o]), ctypes.c_void_p(ws.counts.data_ptr() + 4 * (l + 1)),
-                ctypes.byref(ws.scratch), ctypes.c_void_p(ws.work.data_ptr() + 4 * l),
-                ctypes.byref(opts), sp),
-                "spdnn_layer_forward")
-        evs[L].record()
+        # the whole layer loop in one C call (spdnn_infer_layers_timed), an
+        # event recorded before every layer: launches are not paced by Python
+        handles = evs
+        _native.check(lib.spdnn_infer_layers_timed(
+            L, net.layer_devs, engine._dptr(net.bias), engine._dptr(ws.y[0]),
+            engine._dptr(ws.y[1]), ws.ld, engine._dptr(ws.a[0]), engine._dptr(ws.a[1]),
+            engine._dptr(ws.cat[0]), engine._dptr(ws.cat[1]), engine._dptr(ws.counts),
+            ctypes.byref(ws.scratch), ctypes.byref(opts), sp, handles),
+            "spdnn_infer_layers_timed")
         return engine.DeviceRun(ws, L, m)
 
     # correctness of the timed configuration: categories after one step
@@ -593,12 +591,17 @@ def run_ours(args, cfg):
 
     # ---- timed region (device): K steps, per-launch events around every layer
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(L + 1)] for _ in range(args.steps)]
+    for row in evs:  # create the CUDA events outside the timed region
+        for e in row:
+            e.record()
+    torch.cuda.synchronize()
+    ev_handles = [(ctypes.c_void_p * (L + 1))(*[e.cuda_event for e in row]) for row in evs]
     e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clocks:
         torch.cuda.synchronize()
         e_start.record()
         for k in range(args.steps):
-            step(evs[k])
+            step(ev_handles[k])
         e_end.record()
         torch.cuda.synchronize()
     ms_total = e_start.elapsed_time(e_end)
@@ -801,10 +804,15 @@ def main():
                     help="inputs in the CPU-baseline sample (0 = skip the CPU leg)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="grow the CPU sample to about this much CPU time (0 = fixed sample)")
+    ap.add_argument("--inputs", type=int, default=0,
+                    help="override the batch size (diagnostics: e.g. one rank's share at N=8)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")
     cfg = CONFIGS[args.config]
+    if args.inputs > 0:
+        cfg = dict(cfg, inputs=args.inputs,
+                   name=cfg["name"] + f" [diagnostic: {args.inputs} inputs]")
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

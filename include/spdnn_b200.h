@@ -200,6 +200,15 @@ int spdnn_infer_layers(int64_t num_layers, const spdnn_layer_dev *layers,
                        int32_t *counts, const spdnn_scratch *scratch,
                        const spdnn_run_opts *opts, void *stream);
 
+/* spdnn_infer_layers with a cudaEvent_t recorded on `stream` before every
+ * layer (events[l]) and after the last (events[num_layers]): per-layer device
+ * times without host round trips between launches (measurement). */
+int spdnn_infer_layers_timed(int64_t num_layers, const spdnn_layer_dev *layers,
+                             const float *bias, float *y0, float *y1, int64_t ld,
+                             int32_t *a0, int32_t *a1, int64_t *cat0, int64_t *cat1,
+                             int32_t *counts, const spdnn_scratch *scratch,
+                             const spdnn_run_opts *opts, void *stream, void *const *events);
+
 /* x: float[m][n] feature-major (FeatureBatch.data bytes) -> y: float[n][ld].
  * If guard != NULL: bit 0 |= some 0 < |x| < tiny or |x| > huge, bit 1 |= some
  * x is NaN or inf. */

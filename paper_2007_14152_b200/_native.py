@@ -106,6 +106,9 @@ def lib():
                                           ctypes.POINTER(RunOpts), P]
         L.spdnn_infer_layers.argtypes = [i64, P, P, P, P, i64, P, P, P, P, P,
                                          ctypes.POINTER(Scratch), ctypes.POINTER(RunOpts), P]
+        L.spdnn_infer_layers_timed.argtypes = [i64, P, P, P, P, i64, P, P, P, P, P,
+                                               ctypes.POINTER(Scratch), ctypes.POINTER(RunOpts),
+                                               P, P]
         L.spdnn_transpose_in.argtypes = [P, i64, i64, P, i64, P, ctypes.c_float,
                                          ctypes.c_float, P]
         L.spdnn_gather_out.argtypes = [P, i64, i64, P, P, i64, P, P]
@@ -115,6 +118,7 @@ def lib():
         L.spdnn_version.restype = ctypes.c_char_p
         for name in ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
                      "spdnn_plan_export", "spdnn_layer_forward", "spdnn_infer_layers",
+                     "spdnn_infer_layers_timed",
                      "spdnn_transpose_in", "spdnn_gather_out"):
             getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -134,6 +138,7 @@ def check(rc: int, what: str) -> None:
 # every symbol include/spdnn_b200.h declares (tests check the exports)
 EXPORTED = ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
             "spdnn_plan_export", "spdnn_plan_free", "spdnn_layer_forward",
-            "spdnn_infer_layers", "spdnn_transpose_in", "spdnn_gather_out",
+            "spdnn_infer_layers", "spdnn_infer_layers_timed", "spdnn_transpose_in",
+            "spdnn_gather_out",
             "spdnn_layer_occupancy", "spdnn_profile_read", "spdnn_last_error",
             "spdnn_version")

@@ -118,7 +118,11 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
                : "memory");
 }
 // Blocks (suspended, up to the time hint) until the phase with `parity` is done.
+#ifndef SPDNN_WAIT_HINT_NS
+#define SPDNN_WAIT_HINT_NS 0  // 0: try_wait without a suspend-time hint
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#if SPDNN_WAIT_HINT_NS > 0
   asm volatile(
       "{\n"
       " .reg .pred p;\n"
@@ -126,8 +130,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       " @!p bra WAIT_%=;\n"
       "}\n" ::"r"(bar),
-      "r"(parity), "r"(1000000)
+      "r"(parity), "r"(SPDNN_WAIT_HINT_NS)
       : "memory");
+#else
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bar),
@@ -656,12 +671,19 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     };
     PROF_DECL
     int claim = 0;
+    // entries 0..kMetaAhead are dealt statically, round j giving CTA c item
+    // j*G + ((c + 17j) mod G): a small layer (few items) is spread over all
+    // SMs instead of a few CTAs claiming the lookahead depth each, and the
+    // per-round rotation keeps a CTA from meeting the same block every round
+    // when the block count divides G. Later entries are claimed dynamically
+    // (load balance at the tail) from item (kMetaAhead+1)*G on, so a CTA's
+    // items stay increasing (the first one past the end stops the producer).
+    const int G = (int)gridDim.x;
+    const int dyn0 = (kMetaAhead + 1) * G;
     if (ptid == 0) {
-      // entries 0..kMetaAhead in one claim (a CTA's items must be increasing:
-      // the first one past the end stops the producer), then one per entry
-      const int base = atomicAdd(A.work, kMetaAhead + 1);
-      for (int j = 0; j <= kMetaAhead; j++) s_items[j] = base + j;
-      claim = atomicAdd(A.work, 1);  // entry kMetaAhead + 1
+      for (int j = 0; j <= kMetaAhead; j++)
+        s_items[j] = j * G + (int)((blockIdx.x + 17u * j) % (unsigned)G);
+      claim = dyn0 + atomicAdd(A.work, 1);  // entry kMetaAhead + 1
     }
     pbar();
     for (int j = 0; j < kMetaAhead; j++) {
@@ -680,7 +702,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       // descriptor (group k - 2)
       if (ptid == 0) {
         s_items[(k + kMetaAhead + 1) & 7] = claim;  // claimed one iteration ago
-        claim = atomicAdd(A.work, 1);                // entry k + kMetaAhead + 2
+        claim = dyn0 + atomicAdd(A.work, 1);         // entry k + kMetaAhead + 2
       }
       cp_async_wait<1>();
       pbar();
@@ -1016,6 +1038,16 @@ struct DevInfo {
 };
 DevInfo g_dev;
 
+struct LaunchCache {
+  struct Entry {
+    size_t smem_set = 0;                 // largest dynamic smem size set on the kernel
+    std::map<size_t, int> occ;           // smem size -> CTAs per SM
+  };
+  std::mutex mu;
+  std::map<std::pair<int, const void *>, Entry> map;
+};
+LaunchCache g_launch;
+
 int device_info(int &sms, size_t &optin) {
   int dev;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
@@ -1070,12 +1102,31 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   // warp w visits entries w/gpi + j*(C/gpi): when that stride divides nbuf the
   // warp consumed entry k - nbuf itself before waiting on k (no stale phase)
   A.simple_wait = (G::kC % gpi == 0 && nbuf % (G::kC / gpi) == 0) ? 1 : 0;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
+  // the smem attribute and the occupancy query cost several microseconds of
+  // host time each; a layer loop launches every ~30 us at small batches, so
+  // both are cached per (device, kernel): the attribute only ever grows
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, G::kThreads, smem);
-  if (e != cudaSuccess || per_sm < 1)
-    return spdnn_fail(SPDNN_ECUDA, "layer: kernel does not fit on an SM");
+  {
+    std::lock_guard<std::mutex> lk(g_launch.mu);
+    LaunchCache::Entry &en = g_launch.map[std::make_pair(g_dev.device, fn)];
+    if (smem > en.smem_set) {
+      cudaError_t e0 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem);
+      if (e0 != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e0));
+      en.smem_set = smem;
+      en.occ.clear();
+    }
+    auto it = en.occ.find(smem);
+    if (it == en.occ.end()) {
+      cudaError_t e0 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, G::kThreads, smem);
+      if (e0 != cudaSuccess || per_sm < 1)
+        return spdnn_fail(SPDNN_ECUDA, "layer: kernel does not fit on an SM");
+      en.occ[smem] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
+  cudaError_t e;
   void *args[] = {&A};
   e = cudaLaunchKernel(fn, dim3(sms * per_sm), dim3(G::kThreads), args, smem, stream);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
@@ -1242,11 +1293,11 @@ extern "C" int spdnn_layer_forward(const spdnn_layer_dev *layer, const float *bi
                  scratch, work, opts, stream);
 }
 
-extern "C" int spdnn_infer_layers(int64_t num_layers, const spdnn_layer_dev *layers,
-                                  const float *bias, float *y0, float *y1, int64_t ld,
-                                  int32_t *a0, int32_t *a1, int64_t *cat0, int64_t *cat1,
-                                  int32_t *counts, const spdnn_scratch *scratch,
-                                  const spdnn_run_opts *opts, void *stream) {
+static int infer_layers(int64_t num_layers, const spdnn_layer_dev *layers, const float *bias,
+                        float *y0, float *y1, int64_t ld, int32_t *a0, int32_t *a1,
+                        int64_t *cat0, int64_t *cat1, int32_t *counts,
+                        const spdnn_scratch *scratch, const spdnn_run_opts *opts, void *stream,
+                        void *const *events) {
   if (num_layers < 0 || (num_layers > 0 && (!layers || !scratch)))
     return spdnn_fail(SPDNN_EINVAL, "spdnn_infer_layers: bad argument");
   float *y[2] = {y0, y1};
@@ -1254,11 +1305,36 @@ extern "C" int spdnn_infer_layers(int64_t num_layers, const spdnn_layer_dev *lay
   int64_t *cat[2] = {cat0, cat1};
   for (int64_t l = 0; l < num_layers; l++) {
     int i = (int)(l & 1), o = i ^ 1;
+    if (events && cudaEventRecord((cudaEvent_t)events[l], (cudaStream_t)stream) != cudaSuccess)
+      return spdnn_fail(SPDNN_ECUDA, "spdnn_infer_layers_timed: event record failed");
     int rc = forward(&layers[l], bias, y[i], y[o], ld, a[i], cat[i], counts + l, a[o], cat[o],
                      counts + l + 1, scratch, scratch->work + l, opts, stream);
     if (rc) return rc;
   }
+  if (events && cudaEventRecord((cudaEvent_t)events[num_layers], (cudaStream_t)stream) !=
+                    cudaSuccess)
+    return spdnn_fail(SPDNN_ECUDA, "spdnn_infer_layers_timed: event record failed");
   return SPDNN_OK;
+}
+
+extern "C" int spdnn_infer_layers(int64_t num_layers, const spdnn_layer_dev *layers,
+                                  const float *bias, float *y0, float *y1, int64_t ld,
+                                  int32_t *a0, int32_t *a1, int64_t *cat0, int64_t *cat1,
+                                  int32_t *counts, const spdnn_scratch *scratch,
+                                  const spdnn_run_opts *opts, void *stream) {
+  return infer_layers(num_layers, layers, bias, y0, y1, ld, a0, a1, cat0, cat1, counts, scratch,
+                      opts, stream, nullptr);
+}
+
+extern "C" int spdnn_infer_layers_timed(int64_t num_layers, const spdnn_layer_dev *layers,
+                                        const float *bias, float *y0, float *y1, int64_t ld,
+                                        int32_t *a0, int32_t *a1, int64_t *cat0, int64_t *cat1,
+                                        int32_t *counts, const spdnn_scratch *scratch,
+                                        const spdnn_run_opts *opts, void *stream,
+                                        void *const *events) {
+  if (!events) return spdnn_fail(SPDNN_EINVAL, "spdnn_infer_layers_timed: null events");
+  return infer_layers(num_layers, layers, bias, y0, y1, ld, a0, a1, cat0, cat1, counts, scratch,
+                      opts, stream, events);
 }
 
 extern "C" int spdnn_transpose_in(const float *x, int64_t n, int64_t m, float *y, int64_t ld,

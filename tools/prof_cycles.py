@@ -23,6 +23,8 @@ from paper_2007_14152_b200.model import InferenceConfig  # noqa: E402
 _native.build(force=True)
 cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "c2"]
 plan = sys.argv[sys.argv.index("--plan") + 1] if "--plan" in sys.argv else ""
+if "--inputs" in sys.argv:
+    cfg = dict(cfg, inputs=int(sys.argv[sys.argv.index("--inputs") + 1]))
 params = engine.PlanParams(**{k: int(v) for k, v in (kv.split("=") for kv in plan.split(",") if kv)})
 model, inputs = bench.build_workload(cfg)
 prepared = engine.prepare_model(model, InferenceConfig(), "optimized", params=params)
