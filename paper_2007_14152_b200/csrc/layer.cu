@@ -50,6 +50,10 @@
 namespace {
 
 constexpr int kMaxBufs = 4;
+#ifndef SPDNN_PDL
+#define SPDNN_PDL 1  // programmatic dependent launch between consecutive layers
+#endif
+constexpr int kUsePdl = SPDNN_PDL;
 constexpr int kMetaAhead = 5;  // producer: block descriptors prefetched this many items ahead
 constexpr int kFpAhead = 3;    // producer: staged-row lists prefetched this many items ahead
 constexpr int kMetaRing = 7;   // metadata ring entries (> kMetaAhead)
@@ -595,11 +599,20 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   using G = Geo<FPL, MASK>;
   constexpr int RW = MASK ? 1 : Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int M = *A.m_in;
-  if (M <= 0) return;
+  // Programmatic dependent launch: the next layer's grid may be scheduled as
+  // soon as every CTA here got this far (its CTAs start as SMs free up and run
+  // their static prologue under this layer's tail). Everything the previous
+  // layer wrote -- m_in, a_in, cat_in, y_in, the tile scratch -- is read only
+  // after griddepcontrol.wait (dep_wait below).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int nb = (int)A.L.num_blocks;
-  const int tiles = (M + T - 1) / T;
-  const int items = tiles * nb;
+  int M = 0, tiles = 0, items = 0x7fffffff;  // set by dep_wait
+  auto dep_wait = [&]() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    M = *A.m_in;
+    tiles = (M + T - 1) / T;
+    items = tiles * nb;
+  };
   const int nbuf = A.nbuf, gpi = A.gpi;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
@@ -617,6 +630,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  if (warp < C || warp >= C + P) {
+    dep_wait();
+    if (M <= 0) return;
+  }
 
   if (warp >= C && warp < C + P) {
     // ======================= producer warps =======================
@@ -647,16 +664,18 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     auto ment = [&](int j) { return mring + (j % kMetaRing) * A.mentry_bytes; };
     // entry layout: int desc[8] | int ain[T] | int fp[fpcap]
     auto item_of = [&](int j) { return s_items[j & 7]; };
-    auto prefetch_desc = [&](int j) {  // descriptor + feature columns of item j
+    // descriptor (static: the layer's plan) and feature columns (written by
+    // the previous layer) of item j
+    auto prefetch_desc = [&](int j, bool blk, bool ain) {
       const int item = item_of(j);
       if (item >= items) return;
       const int t = item / nb, b = item - (item / nb) * nb;
       const uint32_t e = (uint32_t)__cvta_generic_to_shared(ment(j));
       if (ptid < 2) {
-        cp_async16(e + 16 * ptid, A.L.blocks + (int64_t)b * 8 + 4 * ptid);
+        if (blk) cp_async16(e + 16 * ptid, A.L.blocks + (int64_t)b * 8 + 4 * ptid);
       } else if (ptid < 2 + T / 4) {
         const int q = ptid - 2;  // a_in has ld >= (t+1)*T entries; lanes past M are masked
-        cp_async16(e + 32 + 16 * q, A.a_in + t * T + 4 * q);
+        if (ain) cp_async16(e + 32 + 16 * q, A.a_in + t * T + 4 * q);
       }
     };
     auto prefetch_fp = [&](int j) {  // staged-row list of item j (descriptor landed)
@@ -686,15 +705,22 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       claim = dyn0 + atomicAdd(A.work, 1);  // entry kMetaAhead + 1
     }
     pbar();
-    for (int j = 0; j < kMetaAhead; j++) {
-      prefetch_desc(j);
-      cp_async_commit();
-    }
+    // static prologue (the plan only), overlapping the previous layer's tail
+    for (int j = 0; j < kMetaAhead; j++) prefetch_desc(j, true, false);
+    cp_async_commit();
     cp_async_wait<0>();
     pbar();
     for (int j = 0; j < kFpAhead; j++) prefetch_fp(j);
     cp_async_commit();
+    dep_wait();
+    if (M <= 0) {
+      cp_async_wait<0>();
+      return;
+    }
+    for (int j = 0; j < kMetaAhead; j++) prefetch_desc(j, false, true);
+    cp_async_commit();
     cp_async_wait<0>();
+    pbar();
     for (int k = 0;; k++) {
       // item k: descriptor (group k - kMetaAhead) and staged rows (group
       // k - kFpAhead) have landed once at most one group (the newest) is
@@ -838,7 +864,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       // metadata for items k + kMetaAhead (descriptor) and k + kFpAhead
       // (staged rows; its descriptor landed with this iteration's wait):
       // ring entry k's slot is reused by k + kMetaRing > k + kMetaAhead only
-      prefetch_desc(k + kMetaAhead);
+      prefetch_desc(k + kMetaAhead, true, true);
       prefetch_fp(k + kFpAhead);
       cp_async_commit();
       pbar();  // every producer's copies issued and counted
@@ -1128,7 +1154,17 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   }
   cudaError_t e;
   void *args[] = {&A};
-  e = cudaLaunchKernel(fn, dim3(sms * per_sm), dim3(G::kThreads), args, smem, stream);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms * per_sm);
+  cfg.blockDim = dim3(G::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = kUsePdl;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   return SPDNN_OK;
 }
