@@ -318,7 +318,7 @@ def run_ours_multi(args, cfg):
     edges_per_input = int(sum(net.nnz))
     shard = parallel.DeviceShard(net, n, m_cap, L, unpadded=unpadded)
     x_dev = pinned.to(dev)
-    c_dev = torch.from_numpy(np.ascontiguousarray(shard_batch.categories)).to(dev)
+    c_dev = engine.host_tensor(np.ascontiguousarray(shard_batch.categories)).to(dev)
     transport = parallel.DistTransport(None, dev)
     thr = InferenceConfig().rebalance_threshold
 
@@ -554,7 +554,7 @@ def run_ours(args, cfg):
     L = net.num_layers
     ws = engine.workspace(n, m, L)
     x_dev = pinned.to(dev)
-    cats_dev = torch.from_numpy(np.ascontiguousarray(batch.categories)).to(dev)
+    cats_dev = engine.host_tensor(np.ascontiguousarray(batch.categories)).to(dev)
     stream = torch.cuda.current_stream()
     opts = engine.run_opts(net)
 

@@ -229,6 +229,17 @@ def _torch():
     return torch
 
 
+def host_tensor(a: np.ndarray):
+    """torch view of a host array without a copy. FeatureBatch arrays are
+    read-only (model.py freezes them); torch only reads them (H2D copies), so
+    its non-writable-array warning is silenced here."""
+    torch = _torch()
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(a)
+
+
 def _dptr(t) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
 
@@ -633,8 +644,8 @@ def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
     if net.num_layers == 0 or m == 0:
         return _trivial_result(net.num_layers, inputs, edges // max(inputs.total_inputs, 1))
     ws = workspace(n, m, net.num_layers)
-    x = torch.from_numpy(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
-    cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
+    x = host_tensor(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
+    cats = host_tensor(np.ascontiguousarray(inputs.categories))
     fma = None
     elapsed = device = 0.0
     for _attempt in range(3):
@@ -726,8 +737,8 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
             pb = _PipeBuffers(n, cap, chunks, L, torch.device("cuda", dev))
             _pipe_cache[key] = pb
     ws = pb.ws
-    host = torch.from_numpy(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
-    cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
+    host = host_tensor(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
+    cats = host_tensor(np.ascontiguousarray(inputs.categories))
     main, up = torch.cuda.current_stream(), pb.up
     lib = _native.lib()
     opts = run_opts(net)
@@ -856,8 +867,8 @@ def _infer_streaming(model: NetworkModel, inputs: FeatureBatch, config: Inferenc
         return _trivial_result(L, inputs, edges)
     bias = np.asarray(model.bias, np.float32)
     ws = workspace(n, m, L)
-    x = torch.from_numpy(np.asarray(inputs.data).T)
-    cats = torch.from_numpy(np.ascontiguousarray(inputs.categories))
+    x = host_tensor(np.asarray(inputs.data).T)
+    cats = host_tensor(np.ascontiguousarray(inputs.categories))
     stage_inputs(ws, x, cats, None)  # tiny = 0: screens only non-finite inputs
     ws.counts.zero_()
     ws.counts[0] = m
@@ -970,7 +981,7 @@ def _one_layer(features: FeatureBatch, prepared: PreparedLayer, bias: np.ndarray
         return np.zeros((n, 0), np.float32, order="F"), np.zeros(0, bool)
     net = DeviceNetwork([prepared], bias)
     ws = Workspace(n, m, 1, torch.device("cuda", torch.cuda.current_device()))
-    x = torch.from_numpy(np.asarray(features.data).T)
+    x = host_tensor(np.asarray(features.data).T)
     fma = None
     for _attempt in range(3):
         stage_inputs(ws, x, torch.arange(m, dtype=torch.int64), net)

@@ -715,8 +715,8 @@ def run_batch_parallel_device(net, inputs: FeatureBatch, config: InferenceConfig
                 raise ModelError("inputs are not this rank's shard of the batch")
             cols = slice(0, hi - lo)
         sh = DeviceShard(net, net.neurons, m_cap, net.num_layers, unpadded=unpadded)
-        x = torch.from_numpy(np.ascontiguousarray(data[:, cols].T))
-        sh.load(x, torch.from_numpy(np.ascontiguousarray(inputs.categories[cols])))
+        x = engine.host_tensor(np.ascontiguousarray(data[:, cols].T))
+        sh.load(x, engine.host_tensor(np.ascontiguousarray(inputs.categories[cols])))
         shards[r] = sh
     torch.cuda.synchronize()
     t0 = time.perf_counter()
