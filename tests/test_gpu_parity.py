@@ -387,3 +387,18 @@ def test_pipelined_upload_matches_single_pass(cuda_ok):
     a = engine.infer(model, poisoned, InferenceConfig(), values=False)
     b = engine.infer(model, poisoned, InferenceConfig())
     assert np.array_equal(a.categories, b.categories)
+
+
+def test_two_features_per_lane_variant(cuda_ok, monkeypatch):
+    """The 64-feature-item kernel variant (FPL = 2, 28 consumer warps) is an
+    alternative launch configuration of the same layout: same bits."""
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=30, connections_per_neuron=32, bias_value=-0.3, seed=12))
+    inputs = ingest.generate_synthetic_inputs(1024, 700, 0.3, seed=13)
+    want = engine.infer(model, inputs, InferenceConfig())
+    monkeypatch.setattr(engine, "FEATURES_PER_LANE", 2)
+    got = engine.infer(model, inputs, InferenceConfig())
+    assert np.array_equal(got.categories, want.categories)
+    assert same_bits(got.final.data, want.final.data)
+    ref = oracle.infer(model, inputs, threads=4)
+    assert got.categories.tolist() == ref.categories.tolist()
