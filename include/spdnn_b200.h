@@ -223,8 +223,9 @@ int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int32_t *a,
 /* Cycle accounting of the layer kernel when the library was built with
  * -DSPDNN_PROFILE (all zero otherwise): out[0..7] consumer-warp clock64 sums
  * (wait for data, record loop, epilogue, bookkeeping), out[8..15] producer
- * warps (empty-slot wait, barrier A, copy issue, metadata, barrier B, tail).
- * Diagnostics only. */
+ * warps (empty-slot wait, barrier A, copy issue, metadata, barrier B, tail),
+ * out[16..21] ring-entry chain sums (issue, fill, consume, release, entries,
+ * releases). n <= 24. Diagnostics only. */
 int spdnn_profile_read(uint64_t *out, int32_t n, int32_t reset);
 
 /* Threadblocks per SM the layer kernel runs with (for diagnostics). */

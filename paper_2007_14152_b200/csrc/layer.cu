@@ -57,9 +57,6 @@ constexpr int kUsePdl = SPDNN_PDL;
 constexpr int kMetaAhead = 5;  // producer: block descriptors prefetched this many items ahead
 constexpr int kFpAhead = 3;    // producer: staged-row lists prefetched this many items ahead
 constexpr int kMetaRing = 7;   // metadata ring entries (> kMetaAhead)
-#ifndef SPDNN_L2_PREFETCH
-#define SPDNN_L2_PREFETCH 0    // L2 prefetch of the next item's staged rows (gather4): measured slower
-#endif
 #ifndef SPDNN_MASK_CONSUMERS
 #define SPDNN_MASK_CONSUMERS 20
 #endif
@@ -169,14 +166,6 @@ __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap *tm
       "r"(bar)
       : "memory");
 }
-// TMA gather4 into L2 only (no shared-memory destination, no completion)
-__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap *tmap, int col, int r0,
-                                                     int r1, int r2, int r3) {
-  asm volatile(
-      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n"
-      ::"l"(reinterpret_cast<uint64_t>(tmap)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-      : "memory");
-}
 // TMA bulk copy global -> this CTA's shared memory, completion as tx bytes
 __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32_t bytes,
                                          uint32_t bar) {
@@ -191,6 +180,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t sdst, const void *gsrc, uint32
 // g_prof at exit: consumers [0..7], producers [8..15]; read and reset with
 // spdnn_profile_read().
 __device__ unsigned long long g_prof[16];
+// ring-chain timings (SPDNN_PROFILE): [0] issue (slot granted -> header posted),
+// [1] fill (posted -> first consumer has data), [2] consume (first consumer ->
+// last unit arrived), [3] release (last unit -> producer regains the slot),
+// [4] entries, [5] releases; SM-local clock64 differences summed over entries
+__device__ unsigned long long g_chain[8];
 #ifdef SPDNN_PROFILE
 #define PROF_DECL                          \
   unsigned long long pf_[8] = {0};         \
@@ -594,6 +588,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs], s_free[kMaxBufs];
   __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ float s_wmask;
+#ifdef SPDNN_PROFILE
+  __shared__ long long s_tgr[kMaxBufs], s_tpost[kMaxBufs], s_tempty[kMaxBufs];
+  __shared__ unsigned long long s_tfirst[kMaxBufs];
+#endif
   __shared__ int s_items[8];  // producer: item index of ring entry j (j & 7)
 
   using G = Geo<FPL, MASK>;
@@ -780,6 +778,17 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const int slot = k % nbuf;
       const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
       if (pw == 0) mbar_wait(free0 + 8 * slot, phase ^ 1u);  // others park at the bar.sync below
+#ifdef SPDNN_PROFILE
+      if (ptid == 0) {
+        const long long now = clock64();
+        if (k >= nbuf) {
+          atomicAdd(&g_chain[3], (unsigned long long)(now - s_tempty[slot]));
+          atomicAdd(&g_chain[5], 1ull);
+        }
+        s_tgr[slot] = now;
+        s_tfirst[slot] = ~0ull;
+      }
+#endif
       PROF_MARK(0);  // [0] waiting for an empty slot
       const uint32_t full = full0 + 8 * slot;
       const uint32_t buf = sbase + slot * A.buf_bytes;
@@ -803,8 +812,24 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       if (ptid == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
       if (ptid == 32 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
       PROF_MARK(2);  // [2] bulk copies of meta + records
+      auto post_header = [&]() {
+        Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
+        h->item = item;
+        h->entry = k;
+        h->t = t;
+        h->b = b;
+        h->nst = nst;
+        h->ng = ng;
+        h->rec_cnt = rec_cnt;
+        h->fp_cnt = fp_cnt;
+#ifdef SPDNN_PROFILE
+        s_tpost[slot] = clock64();
+#endif
+        mbar_arrive(full);
+      };
 #ifdef SPDNN_ABLATE_STAGE
       if (contig) {  // diagnostics: staged rows are not copied (not expected either)
+        if (ptid == 0) post_header();
       } else
 #endif
       if (contig) {
@@ -819,6 +844,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
           tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c.x, c.y, c.z, c.w, full);
         }
         PROF_MARK(6);  // [6] TMA gather4 issue (contiguous tiles)
+        // every byte of the fill was expected up front, so the arrival can go
+        // before the other producers finish issuing: the phase completes only
+        // once all of them have landed
+        if (ptid == 0) post_header();
       } else {
         // staged rows s = 32 pw .. : the warp's 32 lanes copy the row's T features
         for (int s0 = pw * 32; s0 < fp_cnt; s0 += P * 32) {
@@ -834,53 +863,16 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         }
         mbar_cp_async_arrive_inc(full);
         PROF_MARK(7);  // [7] 4-byte cp.async gathers (tiles with gaps)
+        pbar();  // every producer's cp.async arrivals counted before the header's
+        if (ptid == 0) post_header();
       }
-#if SPDNN_L2_PREFETCH
-      {
-        // the next item's staged rows into L2: its fill, one slot turnover
-        // from now, then reads L2 instead of DRAM
-        const int nitem = item_of(k + 1);
-        if (nitem < items) {
-          const int *en1 = reinterpret_cast<const int *>(ment(k + 1));
-          const int t1 = nitem / nb;
-          const int fp1 = en1[5];
-          const int v1 = min(T, M - t1 * T);
-          const int q0 = en1[8];
-          bool mc = true;
-#pragma unroll
-          for (int q = 0; q < FPL; q++)
-            mc &= 32 * q + lane >= v1 || en1[8 + 32 * q + lane] == q0 + 32 * q + lane;
-          if (__all_sync(0xffffffffu, mc) && (q0 & 3) == 0 && 4 * qd0 < fp1) {
-            const int *f1 = en1 + 8 + T + 4 * qd0;
-            const int x0 = f1[0];
-            const int x1 = 4 * qd0 + 1 < fp1 ? f1[1] : x0;
-            const int x2 = 4 * qd0 + 2 < fp1 ? f1[2] : x0;
-            const int x3 = 4 * qd0 + 3 < fp1 ? f1[3] : x0;
-            tma_prefetch_gather4(&A.tmap_in, q0, x0, x1, x2, x3);
-          }
-        }
-      }
-#endif
       // metadata for items k + kMetaAhead (descriptor) and k + kFpAhead
       // (staged rows; its descriptor landed with this iteration's wait):
-      // ring entry k's slot is reused by k + kMetaRing > k + kMetaAhead only
+      // ring entry k's slot is reused by k + kMetaRing > k + kMetaAhead only.
+      // Issued after the header went out: off the slot turnaround path.
       prefetch_desc(k + kMetaAhead, true, true);
       prefetch_fp(k + kFpAhead);
       cp_async_commit();
-      pbar();  // every producer's copies issued and counted
-      PROF_MARK(4);  // [4] barrier B
-      if (ptid == 0) {
-        Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
-        h->item = item;
-        h->entry = k;
-        h->t = t;
-        h->b = b;
-        h->nst = nst;
-        h->ng = ng;
-        h->rec_cnt = rec_cnt;
-        h->fp_cnt = fp_cnt;
-        mbar_arrive(full);
-      }
       PROF_MARK(5);  // [5] header
     }
     PROF_FLUSH(8)
@@ -903,6 +895,17 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const int t = reinterpret_cast<const volatile Header *>(smem + slot * A.buf_bytes)->t;
       if (item < 0) break;
       mbar_wait(empty0 + 8 * slot, phase);
+#ifdef SPDNN_PROFILE
+      if (lane == 0) {
+        const long long now = clock64();
+        const long long first = (long long)s_tfirst[slot];
+        atomicAdd(&g_chain[0], (unsigned long long)(s_tpost[slot] - s_tgr[slot]));
+        atomicAdd(&g_chain[1], (unsigned long long)(first - s_tpost[slot]));
+        atomicAdd(&g_chain[2], (unsigned long long)(now - first));
+        atomicAdd(&g_chain[4], 1ull);
+        s_tempty[slot] = now;
+      }
+#endif
       uint32_t wv = lane < FPL ? s_alive[slot][lane] : 0u;
       if (lane < FPL) s_alive[slot][lane] = 0u;
       __syncwarp();
@@ -985,6 +988,9 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     }
     const Header h = *reinterpret_cast<const Header *>(buf);
     PROF_MARK(0);  // [0] waiting for data
+#ifdef SPDNN_PROFILE
+    if (lane == 0 && h.item >= 0) atomicMin(&s_tfirst[slot], (unsigned long long)clock64());
+#endif
     if (h.item < 0) break;
     if (g < h.ng) {
       const int32_t *meta = reinterpret_cast<const int32_t *>(buf + kHeaderBytes);
@@ -1002,7 +1008,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         accumulate_mask<R, FMA, FPL>(acc, recs + meta[seg_base + 2 * g],
                                      meta[seg_base + 2 * g + 1],
                                      (uint32_t)__cvta_generic_to_shared(ybase), w_mask, negz2);
-      } else {
+      } else if (!MASK) {
         accumulate<R, FMA, FPL, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
                                    meta[seg_base + 2 * g + 1], ybase, negz2);
       }
@@ -1395,14 +1401,16 @@ extern "C" int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int
 }
 
 extern "C" int spdnn_profile_read(uint64_t *out, int32_t n, int32_t reset) {
-  if (!out || n < 0 || n > 16) return spdnn_fail(SPDNN_EINVAL, "spdnn_profile_read: bad args");
-  unsigned long long h[16];
-  cudaError_t e = cudaMemcpyFromSymbol(h, g_prof, sizeof(h));
+  if (!out || n < 0 || n > 24) return spdnn_fail(SPDNN_EINVAL, "spdnn_profile_read: bad args");
+  unsigned long long h[24];
+  cudaError_t e = cudaMemcpyFromSymbol(h, g_prof, 16 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemcpyFromSymbol(h + 16, g_chain, 8 * sizeof(unsigned long long));
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   for (int i = 0; i < n; i++) out[i] = h[i];
   if (reset) {
     std::memset(h, 0, sizeof(h));
-    e = cudaMemcpyToSymbol(g_prof, h, sizeof(h));
+    e = cudaMemcpyToSymbol(g_prof, h, 16 * sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_chain, h, 8 * sizeof(unsigned long long));
     if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   }
   return SPDNN_OK;

@@ -45,9 +45,9 @@ ws.a[0][:mi].copy_(ws.iota[:mi])
 opts = engine.run_opts(net)
 lib = _native.lib()
 sp = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-prof = (ctypes.c_uint64 * 16)()
+prof = (ctypes.c_uint64 * 24)()
 torch.cuda.synchronize()
-lib.spdnn_profile_read(prof, 16, 1)
+lib.spdnn_profile_read(prof, 24, 1)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(21)]
 for r in range(21):
     ws.counts[layer] = mi
@@ -66,7 +66,7 @@ ts = [ev[r].elapsed_time(ev[r + 1]) * 1e3 for r in range(20)]
 plan = sys.argv[sys.argv.index("--plan") + 1] if "--plan" in sys.argv else ""
 print(f"{os.environ.get('SPDNN_NVCC_DEFINES', '(default)')} [{plan}]: layer {layer} "
       f"{np.median(ts):.1f} us (M={mi})")
-lib.spdnn_profile_read(prof, 16, 0)
+lib.spdnn_profile_read(prof, 24, 0)
 v = np.array(list(prof), dtype=np.float64)
 if v.sum() > 0:
     c, p = v[:4], v[8:16]
@@ -74,3 +74,8 @@ if v.sum() > 0:
           tuple(c / c.sum() * 100))
     print("  producer %%: empty %.1f barA %.1f bulk %.1f meta %.1f barB %.1f hdr %.1f "
           "gather4 %.1f cpasync %.1f" % tuple(p / p.sum() * 100))
+    ch = v[16:22]
+    if ch[4] > 0:
+        print("  ring entry chain (us @1.965 GHz): issue %.2f fill %.2f consume %.2f release %.2f"
+              % (ch[0] / ch[4] / 1965, ch[1] / ch[4] / 1965, ch[2] / ch[4] / 1965,
+                 ch[3] / max(ch[5], 1) / 1965))
