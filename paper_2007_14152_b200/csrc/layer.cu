@@ -1285,8 +1285,10 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
             int64_t ld, const int32_t *a_in, const int64_t *cat_in, const int32_t *m_in,
             int32_t *a_out, int64_t *cat_out, int32_t *m_out, const spdnn_scratch *scratch,
             int32_t *work, const spdnn_run_opts *opts, void *stream) {
+  // ld * 4 must fit 32 bits: the epilogue forms row addresses with one wide multiply
   if (!layer || !bias || !y_in || !y_out || !a_in || !cat_in || !m_in || !a_out ||
-      !cat_out || !m_out || !scratch || !work || ld < 1 || ld % SPDNN_TILE_FEATURES)
+      !cat_out || !m_out || !scratch || !work || ld < 1 || ld % SPDNN_TILE_FEATURES ||
+      ld >= (int64_t)1 << 30)
     return spdnn_fail(SPDNN_EINVAL, "spdnn_layer_forward: bad argument");
   const bool fma = opts && opts->fma_form;
   if (fma && !scratch->guard)
