@@ -106,6 +106,57 @@ def test_wrong_mode_prepared_raises(cuda_ok):
         parallel.run_batch_parallel(model, inputs, cfg, mode="optimized", prepared=bad)
 
 
+def _dist_worker_shard_only(rank, world, port, q):
+    """Each rank builds the network chunk-wise and holds only its own shard
+    (run_batch_parallel_device(shard_only=True), the bench's N > 1 path)."""
+    import os
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = ingest.GeneratorSpec(neurons=1024, layers=40, connections_per_neuron=32,
+                                    bias_value=-0.3, seed=21)
+        net = engine.DeviceNetwork.from_layers(ingest.iter_synthetic_layers(spec),
+                                               ingest.synthetic_bias(spec), chunk=7)
+        lo, hi = parallel.shard_bounds(900, world)[rank]
+        shard = ingest.generate_synthetic_inputs(1024, 900, 0.3, seed=22, columns=(lo, hi))
+        res, comm, bal = parallel.run_batch_parallel_device(
+            net, shard, InferenceConfig(workers=world), values=True, shard_only=True)
+        q.put((rank, res.categories.tolist(),
+               [(o.active_before, o.active_after) for o in res.per_layer],
+               np.asarray(res.final.data).view(np.uint32).tobytes(), res.edges_processed))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_shard_only_two_ranks_chunk_built(cuda_ok):
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dist_worker_shard_only, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=40, connections_per_neuron=32, bias_value=-0.3, seed=21))
+    inputs = ingest.generate_synthetic_inputs(1024, 900, 0.3, seed=22)
+    single = engine.infer(model, inputs, InferenceConfig())
+    for rank, cats, per_layer, vbits, edges in res:
+        assert cats == single.categories.tolist()
+        assert per_layer == [(o.active_before, o.active_after) for o in single.per_layer]
+        assert vbits == np.asarray(single.final.data).view(np.uint32).tobytes()
+        assert edges == single.edges_processed
+
+
 def _dist_worker(rank, world, port, q):
     import os
     import torch
