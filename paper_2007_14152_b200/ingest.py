@@ -84,7 +84,10 @@ def layer_parameters(neurons: int, layers: int, seed: int) -> list[tuple[int, in
 def synthetic_layer(neurons: int, k: int, offset: int, stride: int) -> LayerCSR:
     """Row r -> sorted {(r*offset + i*stride) mod N}, all weights 1/16."""
     base = (np.arange(neurons, dtype=np.int64) * offset) % neurons
-    cols = (base[:, None] + (np.arange(k, dtype=np.int64) * stride)[None, :]) % neurons
+    # base + i*stride < (k + 1) * N: int32 when that fits (sorting 3x faster)
+    dt = np.int32 if (k + 1) * neurons < 2 ** 31 else np.int64
+    cols = (base.astype(dt)[:, None] + (np.arange(k, dtype=np.int64) * stride).astype(dt)[None, :]) \
+        % dt(neurons)
     cols.sort(axis=1)
     return LayerCSR(row_ptr=np.arange(0, neurons * k + 1, k, dtype=np.int64),
                     col_idx=cols.reshape(-1).astype(np.int32),
