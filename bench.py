@@ -183,7 +183,8 @@ def cpu_baseline(model, inputs, sample_cols: int, threads: int, target_s: float 
     r = oracle.infer(model, sub, threads=threads, want_final=False)
     dt = time.perf_counter() - t0
     edges = sample_cols * sum(l.nnz for l in model.layers)
-    return dict(value=edges / dt / 1e12, seconds=dt, counts=r.counts, sample_cols=sample_cols)
+    return dict(value=edges / dt / 1e12, seconds=dt, counts=r.counts, sample_cols=sample_cols,
+                categories=r.categories)
 
 
 def run_reference_streamed(args, cfg):
@@ -426,17 +427,31 @@ def resident_workload(args, cfg, params):
     def e2e(batch):
         return engine.infer(model, batch, InferenceConfig(), prepared=prepared, values=False)
 
+    sample = {}
+
     def cpu(inputs):
         threads = os.cpu_count() or 1
         r = cpu_baseline(model, inputs, args.cpu_sample, threads, target_s=args.cpu_seconds)
+        sample.update(r)
         return {"value": r["value"], "unit": "TE/s", "cores": threads, "kind": "port",
                 "sample": f"first {r['sample_cols']} of {cfg['inputs']} inputs, all "
                           f"{model.num_layers} layers, oracle/spdnn_oracle.c on {threads} "
                           f"host threads ({r['seconds']:.1f} s)"}
 
+    def parity(full_cats):
+        """The timed CPU sample doubles as a full-size parity sample: the GPU
+        run's survivors among the first sample_cols inputs must be exactly the
+        oracle's (features never interact, so a prefix is a valid sample)."""
+        if not sample:
+            return None
+        n_s = sample["sample_cols"]
+        got = np.asarray(full_cats)[np.asarray(full_cats) < n_s]
+        return {"sample_columns": int(n_s), "survivors_in_sample": int(len(sample["categories"])),
+                "bit_exact": bool(np.array_equal(got, sample["categories"]))}
+
     return Workload(net=net, nnz=np.array([l.nnz for l in model.layers], np.float64),
                     e2e=e2e, e2e_path="engine.infer(values=False) on a pinned-host FeatureBatch",
-                    cpu=cpu, parity=None)
+                    cpu=cpu, parity=parity, parity_after_cpu=True)
 
 
 class StreamedOracle:
@@ -524,7 +539,7 @@ def chunked_workload(args, cfg, params, batch):
         return {"sample_columns": len(cols), "survivors_in_sample": len(orc.cats),
                 "bit_exact": bool(ok)}
 
-    return Workload(net=net, nnz=np.asarray(net.nnz, np.float64), e2e=e2e,
+    return Workload(net=net, nnz=np.asarray(net.nnz, np.float64), e2e=e2e, parity_after_cpu=False,
                     e2e_path="engine.infer_device(values=False) on a pinned-host FeatureBatch "
                              "(network resident, built by DeviceNetwork.from_layers)",
                     cpu=cpu, parity=parity)
@@ -646,12 +661,13 @@ def run_ours(args, cfg):
     assert np.array_equal(res.categories, cats_chk.cpu().numpy()), "e2e categories differ"
     h2d = m * n * 4 + m * 8
     d2h = len(res.categories) * 8 + (L + 1) * 4
-    parity = W.parity(res.categories) if W.parity else None
+    parity = W.parity(res.categories) if W.parity and not W.parity_after_cpu else None
+    cpu = W.cpu(batch) if args.cpu_sample > 0 else None
+    if W.parity and W.parity_after_cpu:
+        parity = W.parity(res.categories)
     if parity is not None:
         log(f"full-size sampled parity: {parity}")
         assert parity["bit_exact"], "GPU differs from the oracle on the sampled columns"
-
-    cpu = W.cpu(batch) if args.cpu_sample > 0 else None
     line = {
         "metric": "TeraEdges/s", "value": value, "unit": "TE/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
