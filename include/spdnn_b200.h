@@ -123,9 +123,9 @@ int spdnn_plan_sizes(const spdnn_plan *plan, spdnn_plan_sizes_t *sizes);
  *           (slot * SPDNN_STAGED_ROW_BYTES), words 1..R = fp32 weight bits
  *           per group row (0 = not connected); per group ascending neuron.
  *           Uniform layers (sizes.uniform): one word per record,
- *           slot << 24 | mask (bit k = group row k connects; the weight is
- *           sizes.weight_bits), each group's run padded with zero words to a
- *           multiple of 4
+ *           slot << 24 | mask << 1 (bit k+1 = group row k connects; the
+ *           weight is sizes.weight_bits), each group's run padded with zero
+ *           words to a multiple of 4
  */
 int spdnn_plan_export(const spdnn_plan *plan, int32_t *blocks, int32_t *stages,
                       int32_t *meta, uint32_t *records);

@@ -370,8 +370,8 @@ __device__ __forceinline__ void accumulate(u64 *acc, const uint32_t *recs, int c
 }
 
 // Mask records (uniform weight w): 4 one-word records per 16-byte load; word
-// = staged-row slot << 24 | row mask, so the row's byte offset is word >> 15
-// (one LEA.HI with the base). Rows whose bit is clear add nothing --
+// = staged-row slot << 24 | row mask << 1, so the row's byte offset is
+// word >> 15 (one LEA.HI with the base) and row k is bit k+1. Rows whose bit is clear add nothing --
 // exactly the reference's sum, which never visits those columns. Each
 // group's run is padded to a multiple of 4 with zero words (no-ops).
 template <int R, bool FMA, int FPL>
@@ -380,7 +380,7 @@ __device__ __forceinline__ void mask_record(u64 *acc, uint32_t wd, const YVec<FP
   constexpr int H = FPL / 2;
 #pragma unroll
   for (int k = 0; k < R; k++) {
-    if (wd & (1u << k)) {
+    if (wd & (2u << k)) {  // row k = mask bit k+1
 #pragma unroll
       for (int h = 0; h < H; h++) {
         if (FMA) fma2_acc(acc[H * k + h], y.v[h], w);
@@ -557,8 +557,8 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
         const uint32_t wd = __ldg(recs + i);
         off = wd >> 15;
 #pragma unroll
-        for (int k = 0; k < R; k++) w[k] = (wd >> k) & 1u ? w0 : 0.0f;
-        if ((wd & ((1u << R) - 1u)) == 0u) continue;  // padding word
+        for (int k = 0; k < R; k++) w[k] = (wd >> (k + 1)) & 1u ? w0 : 0.0f;
+        if ((wd & (((1u << R) - 1u) << 1)) == 0u) continue;  // padding word
       } else {
         Rec<R>::load(recs + i * RW, off, w);  // (global loads)
       }

@@ -254,7 +254,9 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
           const float w = row >= 0 ? weight(row, c) : 0.0f;
           uint32_t bits;
           std::memcpy(&bits, &w, 4);
-          if (pl->uniform) pl->records[base] |= (bits != 0u ? 1u : 0u) << k;
+          // row k is mask bit k+1: the kernel turns bits 1..6 into predicates
+          // with one R2P and bit 7 with one LOP3 (bit 0 would cost two ops)
+          if (pl->uniform) pl->records[base] |= (bits != 0u ? 2u : 0u) << k;
           else pl->records[base + 1 + k] = bits;
         }
         cnt++;

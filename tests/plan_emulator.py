@@ -54,12 +54,12 @@ def emulate_layer(plan, bias, x):
                 fp, recs = stages[s]
                 for r in recs[rel:rel + cnt]:
                     if plan.uniform:
-                        # one word: slot << 24 | row mask; unset bits add nothing
+                        # one word: slot << 24 | row mask << 1; unset bits add nothing
                         word = int(r[0])
                         y = x[fp[word >> 24]]
                         w = np.uint32(plan.weight_bits).view(np.float32)
                         for k in range(R):
-                            if word >> k & 1:
+                            if word >> (k + 1) & 1:
                                 acc[k] = acc[k] + (y * w).astype(np.float32)
                         continue
                     assert int(r[0]) % ROW_BYTES == 0
