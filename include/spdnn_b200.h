@@ -57,7 +57,7 @@ enum {
 /* ---- one-time layout conversion (host, C++) ----------------------------- */
 
 typedef struct spdnn_plan_params {
-  int32_t rows_per_group;   /* R in {1, 3, 7}; 0 = choose per layer */
+  int32_t rows_per_group;   /* R in {1, 3, 6, 7}; 0 = choose per layer */
   int32_t footprint_cap;    /* max input neurons staged per block stage */
   int32_t max_groups;       /* max row groups per block (<= warps per CTA) */
   int32_t record_cap;       /* max union records staged per block stage */

@@ -268,6 +268,21 @@ struct Rec<3> {
   }
 };
 template <>
+struct Rec<6> {
+  static constexpr int W = 8;
+  __device__ __forceinline__ static void load(const uint32_t *p, uint32_t &off, float *w) {
+    uint4 a = *reinterpret_cast<const uint4 *>(p);
+    uint4 b = *reinterpret_cast<const uint4 *>(p + 4);
+    off = a.x;
+    w[0] = __uint_as_float(a.y);
+    w[1] = __uint_as_float(a.z);
+    w[2] = __uint_as_float(a.w);
+    w[3] = __uint_as_float(b.x);
+    w[4] = __uint_as_float(b.y);
+    w[5] = __uint_as_float(b.z);
+  }
+};
+template <>
 struct Rec<7> {
   static constexpr int W = 8;
   __device__ __forceinline__ static void load(const uint32_t *p, uint32_t &off, float *w) {
@@ -1058,9 +1073,13 @@ void *kernel_ptr(bool fma) {
 
 template <int FPL, bool MASK>
 void *kernel_for(int R, bool fma) {
-  return R == 1 ? kernel_ptr<1, FPL, MASK>(fma)
-                : (R == 3 ? kernel_ptr<3, FPL, MASK>(fma)
-                          : (R == 7 ? kernel_ptr<7, FPL, MASK>(fma) : nullptr));
+  switch (R) {
+    case 1: return kernel_ptr<1, FPL, MASK>(fma);
+    case 3: return kernel_ptr<3, FPL, MASK>(fma);
+    case 6: return kernel_ptr<6, FPL, MASK>(fma);
+    case 7: return kernel_ptr<7, FPL, MASK>(fma);
+    default: return nullptr;
+  }
 }
 
 struct DevInfo {
@@ -1102,7 +1121,7 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   using G = Geo<FPL, MASK>;
   const spdnn_layer_dev &L = A.L;
   void *fn = kernel_for<FPL, MASK>(L.rows_per_group, fma);
-  if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1, 3 or 7");
+  if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1, 3, 6 or 7");
   if (MASK != (L.uniform != 0) || (MASK && L.record_words != 1))
     return spdnn_fail(SPDNN_EINVAL, "layer: record format does not match the layout");
   int sms;

@@ -47,7 +47,8 @@ def _layer_case(layer, params, rng, m):
 PARAMS = [PlanParams(), PlanParams(rows_per_group=1, reorder=False),
           PlanParams(rows_per_group=3), PlanParams(rows_per_group=7, reorder=False),
           PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3),
-          PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2)]
+          PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2),
+          PlanParams(rows_per_group=6)]
 
 
 @pytest.mark.parametrize("pi", range(len(PARAMS)))

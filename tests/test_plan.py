@@ -21,6 +21,7 @@ PARAMS = [
     PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3),
     PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2, max_groups=16),
     PlanParams(rows_per_group=1, footprint_cap=1, record_cap=1, max_groups=1),
+    PlanParams(rows_per_group=6),
 ]
 
 
