@@ -725,13 +725,25 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     pbar();
     for (int j = 0; j < kFpAhead; j++) prefetch_fp(j);
     cp_async_commit();
-    dep_wait();
+    // the feature columns of the first entries are fetched together with
+    // the active count (one round trip): the tile of a statically dealt item
+    // is known without M, and a tile inside the a_in allocation is safe to
+    // read even if it turns out to lie past M (such items are never filled)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int j = 0; j < kMetaAhead; j++) {
+      const int t0 = item_of(j) / nb;
+      if ((int64_t)(t0 + 1) * T <= A.ld) {
+        const uint32_t e = (uint32_t)__cvta_generic_to_shared(ment(j));
+        if (ptid >= 2 && ptid < 2 + T / 4)
+          cp_async16(e + 32 + 16 * (ptid - 2), A.a_in + t0 * T + 4 * (ptid - 2));
+      }
+    }
+    cp_async_commit();
+    dep_wait();  // (griddepcontrol.wait again: returns at once) + M
     if (M <= 0) {
       cp_async_wait<0>();
       return;
     }
-    for (int j = 0; j < kMetaAhead; j++) prefetch_desc(j, false, true);
-    cp_async_commit();
     cp_async_wait<0>();
     pbar();
     for (int k = 0;; k++) {
