@@ -685,7 +685,24 @@ def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
 
 
 PIPELINE_MIN_FEATURES = 4096  # smallest first chunk of the upload/compute pipeline
-PIPELINE_HEAD = 8             # the first chunk is 1/8 of the batch
+# cost model of the head/rest split (B200 measurements): pinned
+# host->device bandwidth, credited edge rate of the layer loop, fixed cost per
+# layer launch of a chunk
+PIPELINE_H2D_BPS = 50e9
+PIPELINE_EDGE_RATE = 30e12
+PIPELINE_LAYER_FIXED_S = 12e-6
+
+
+def pipeline_head(m: int, neurons: int, num_layers: int, edges_per_input: float) -> int:
+    """Features in the head chunk: large enough that its compute covers the
+    rest's upload (then only the head's upload is exposed), no larger --
+    h = (T_up - T_fixed) / (T_up + T_compute), clamped to [1/16, 1/2]."""
+    t_up = m * neurons * 4.0 / PIPELINE_H2D_BPS
+    t_comp = m * edges_per_input / PIPELINE_EDGE_RATE
+    t_fixed = num_layers * PIPELINE_LAYER_FIXED_S
+    h = (t_up - t_fixed) / max(t_up + t_comp, 1e-12)
+    h = min(0.5, max(1.0 / 16, h))
+    return max(PIPELINE_MIN_FEATURES, int(m * h))
 _pipe_cache: dict = {}
 
 
@@ -713,16 +730,16 @@ class _PipeBuffers:
 def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
     """values=False inference with the input upload overlapped: the batch is
     cut into two feature ranges (features never interact, so each runs the
-    whole network on its own): a head of 1/PIPELINE_HEAD of the batch, whose
-    upload is the only one exposed, and the rest, copied host->device on a
-    side stream while the head's layers run (the head computes for about as
-    long as the rest takes to upload, and only one extra launch per layer is
-    paid). One host synchronisation at the end reads every chunk's counts.
+    whole network on its own): a head (pipeline_head: sized so its compute
+    covers the rest's upload) whose upload is the only one exposed, and the
+    rest, copied host->device on a side stream while the head's layers run;
+    one extra launch per layer is paid. One host synchronisation at the end
+    reads every chunk's counts.
     Returns None when an arithmetic guard fired (the caller then takes the
     unchunked path, which reruns in the exact form)."""
     torch = _torch()
     n, m, L = net.neurons, inputs.active_count, net.num_layers
-    head = max(PIPELINE_MIN_FEATURES, m // PIPELINE_HEAD)
+    head = pipeline_head(m, n, L, edges / max(inputs.total_inputs, 1))
     bounds = [(0, head), (head, m)]
     chunks = 2
     cap = max(hi - lo for lo, hi in bounds)

@@ -15,11 +15,6 @@ for rep in range(4):
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     print(f"e2e {1e3*(t1-t0):.1f} ms; elapsed(in-call clock) {1e3*r.elapsed_seconds:.1f} ms; device {1e3*r.device_seconds:.1f} ms")
-for h in (6, 8, 10, 12):
-    engine.PIPELINE_HEAD = h
-    ts = []
-    for rep in range(3):
-        torch.cuda.synchronize(); t0 = time.perf_counter()
-        r = engine.infer(model, batch, InferenceConfig(), prepared=prepared, values=False)
-        torch.cuda.synchronize(); ts.append(time.perf_counter() - t0)
-    print(f"head 1/{h}: e2e {1e3*np.median(ts):.1f} ms")
+n, L = model.neurons, model.num_layers
+print("head features:", engine.pipeline_head(batch.active_count, n, L,
+                                              sum(l.nnz for l in model.layers)))
