@@ -8,32 +8,34 @@
 //   engine.compact_active       engine.py:130-142  (keep alive features)
 //   engine.infer layer loop     engine.py:264-285
 //
-// Work item = (tile t of 128 active features, row block b of the layer plan).
-// One persistent CTA per SM, warp-specialised:
-//   * 1 producer warp pulls items from a per-layer atomic counter and fills a
-//     ring of shared-memory buffers with cp.async: the block's metadata and
-//     union records (contiguous 16-byte chunks) and, for every staged input
-//     neuron c of the block footprint, the tile's 128 feature values
-//     y_in[c][a_in[128t + f]] (one 16-byte copy per lane when the lane's four
-//     features are contiguous, else four 4-byte gathers). Completion is
-//     tracked by an mbarrier per buffer (cp.async.mbarrier.arrive.noinc);
-//   * 16 consumer warps each own one row group (R output rows) of the item.
-//     Lane l holds features 4l..4l+3 of the tile as two f32x2 register pairs.
-//     Per union record (one input neuron, ascending neuron index): one
-//     LDS.128 of the four values, and per row k two FFMA2 with weight w_k
-//     (0 where row k does not connect). Every row adds its own products in
-//     ascending column order, interleaved with exact +0 terms: bit-equal to
-//     the reference's CSR sum (kernels.py:27-37, separate mul and add):
+// Work item = (tile t of 128 active features, row block b of the layer plan);
+// one item fills one entry of a ring of 2-4 shared-memory buffers. One
+// persistent CTA per SM (launched with programmatic stream serialization, so
+// a layer's static prologue runs under the previous layer's tail), warp
+// roles:
+//   * 3 producer warps: item metadata (block descriptor, the tile's feature
+//     columns, the staged-row list) is prefetched with cp.async into a small
+//     ring several items ahead; per entry one expect_tx, TMA bulk copies of
+//     the block metadata and records, and TMA gather4 of the staged rows
+//     (4 input neurons x 128 features per op) -- or 4-byte cp.async when the
+//     tile's columns have gaps (the layer after deaths);
+//   * 20 consumer warps (mask records; 16 for per-row weight records): one
+//     unit = one row group of the entry. Lane l holds features 4l..4l+3 as
+//     two f32x2 pairs; per record (one input neuron, ascending neuron index)
+//     one LDS.128 of the four values and two FFMA2 per connected row. Every
+//     row adds its own products in ascending column order: bit-equal to the
+//     reference's CSR sum (kernels.py:27-37, separate mul and add):
 //        FMA form  (all weights +-2^e): acc = fma(y, w, acc); y*w is exact,
 //                  so fma == fl(acc + fl(y*w)). Outputs small enough that the
 //                  next layer's products could underflow set a guard bit and
 //                  the engine reruns in the exact form.
 //        exact form (any weights): p = fma(y, w, -0) == fl(y*w); acc += p.
 //     Epilogue: v = fl(acc + bias), comparison clamp (NaN kept,
-//     kernels.py:33-36), 16-byte store of the four features, alive |= v > 0;
-//   * the last consumer warp to finish an item publishes its activity bits;
-//     the item that completes tile t appends the tile's alive features to
-//     a_out / cat_out (pruning without a pass over Y).
+//     kernels.py:33-36), 16-byte store per row, activity bits by ballot;
+//   * 1 publisher warp: once every unit of an entry has arrived, folds the
+//     entry's activity bits into its tile and releases the slot; the item
+//     that completes tile t appends the tile's alive features to a_out /
+//     cat_out (pruning without a pass over Y).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
