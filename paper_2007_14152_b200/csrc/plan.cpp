@@ -15,7 +15,7 @@
 //     interleaved with exact +0 contributions, so its fp32 sum is bit-equal to
 //     the reference's ascending CSR sum (spdnn/kernels.py:27-37);
 //   * consecutive groups form a block whose input footprint (union of the
-//     group unions) is staged once per 64-feature tile; a block whose single
+//     group unions) is staged once per 128-feature tile; a block whose single
 //     group needs more than `footprint_cap` inputs is split into stages
 //     (the reference's buffer_capacity stages, preprocess.py:148-190).
 #include <algorithm>

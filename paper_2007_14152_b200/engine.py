@@ -18,8 +18,8 @@ its own columns -- the analogue of the reference's CSR baseline kernel. The
 two produce bit-identical outputs, as in the reference (kernels.py:1-9).
 
 Device data layout: features are neuron-major,
-``Y[n][j]`` with the 64-feature tiles contiguous, so every staged input
-neuron is one coalesced 256-byte row segment; dead features are dropped by
+``Y[n][j]`` with the 128-feature tiles contiguous, so every staged input
+neuron is one coalesced 512-byte row segment; dead features are dropped by
 index lists that the layer kernel itself appends (no compaction pass).
 """
 
@@ -1036,7 +1036,7 @@ def optimized_layer(features: FeatureBatch, prepared, bias: np.ndarray,
 
     ``prepared`` is a PreparedLayer (or its LayerPlan). ``minibatch`` is
     accepted for signature compatibility (engine.py:109); the kernel's feature
-    tile is fixed at 64.
+    tile is fixed at 128.
     """
     if minibatch is not None and minibatch < 1:
         raise ModelError("minibatch must be positive")
