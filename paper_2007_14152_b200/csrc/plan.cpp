@@ -205,6 +205,28 @@ double record_cost(int R) { return R == 1 ? 3.0 : (R == 3 ? 3.0 : 4.25); }
 // pipe retires 2 FFMA2 per clock per SM (R = 7: 14 FFMA2 = 7 clocks).
 double mask_record_cost(int R) { return R == 7 ? 7.0 : 4.25; }
 
+// The kernel keeps at least two ring entries in shared memory, so one
+// block stage (staged rows + records + metadata + header) must fit half of
+// the ~225 KB a CTA can use. The caps were tuned for one-word mask records;
+// per-row weight records are 2-8 words, so the record cap, then the
+// footprint cap, shrink until a stage fits.
+spdnn_plan_params fit_caps(spdnn_plan_params p, int R, int RW) {
+  // (227 KB - static smem - the producer's metadata ring) / 2, minus the
+  // 128-byte rounding of every region
+  const int64_t budget = 104 * 1024;
+  auto stage_bytes = [&](int64_t s, int64_t rc) {
+    const int64_t meta = s + 4 + 2 * (int64_t)p.max_groups + 2 * (int64_t)R * p.max_groups + 4;
+    return s * SPDNN_STAGED_ROW_BYTES + rc * RW * 4 + 16 + meta * 4 + 128 + 3 * 128;
+  };
+  while (stage_bytes(p.footprint_cap, p.record_cap) > budget && p.record_cap > p.footprint_cap)
+    p.record_cap = std::max(p.footprint_cap, p.record_cap - 8);
+  while (stage_bytes(p.footprint_cap, p.record_cap) > budget && p.footprint_cap > 8) {
+    p.footprint_cap -= 8;
+    p.record_cap = std::max(p.footprint_cap, p.record_cap);
+  }
+  return p;
+}
+
 void pad4(std::vector<int32_t> &v) {
   while (v.size() % 4) v.push_back(0);
 }
@@ -402,7 +424,7 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
     pl->RW = record_words(R, pl->uniform != 0);
     pl->num_groups = (int64_t)best.size();
     pl->pow2 = pow2_weights(pl->nnz, values, pl->wexp_min, pl->wexp_max) ? 1 : 0;
-    emit(pl, row_ptr, col_idx, values, best, p);
+    emit(pl, row_ptr, col_idx, values, best, fit_caps(p, R, pl->RW));
   } catch (const std::bad_alloc &) {
     delete pl;
     return spdnn_fail(SPDNN_ENOMEM, "spdnn_plan_build: out of memory");

@@ -424,3 +424,47 @@ def test_config2_full_size_sampled_columns(cuda_ok):
     assert got.categories.tolist() == ref.categories.tolist()
     assert same_bits(got.final.data, ref.final)
     assert [o.active_before for o in got.per_layer] + [len(got.categories)] == ref.counts.tolist()
+
+
+def _window_layer(rng, n, k, weights):
+    """A row-permuted sliding-window layer (the generator's structure) with
+    arbitrary per-entry weights: the union layout groups it with R = 7 but
+    must use per-row weight records and the exact arithmetic form."""
+    off = int(rng.integers(1, n))
+    st = 1
+    while np.gcd(st, n) != 1:
+        st = int(rng.integers(1, n))
+    base = (np.arange(n, dtype=np.int64) * off) % n
+    cols = (base[:, None] + np.arange(k, dtype=np.int64)[None, :] * st) % n
+    rows = np.repeat(np.arange(n), k)
+    return make_layer_csr(n, rows, cols.reshape(-1), weights(rng, n * k))
+
+
+@pytest.mark.parametrize("kind", ["uniform_negative", "random_pm", "mixed_pow2"])
+def test_medium_structured_networks_all_record_formats(cuda_ok, kind):
+    """2048 neurons x 12 layers x 2500 inputs with sliding-window structure
+    under three weight regimes: one negative value (mask records, FMA form),
+    random +-uniform values (weight records, exact form), powers of two of
+    mixed sign and exponent (weight records, FMA form). Bit-exact vs oracle."""
+    rng = np.random.default_rng({"uniform_negative": 1, "random_pm": 2, "mixed_pow2": 3}[kind])
+    wfn = {
+        "uniform_negative": lambda r, c: np.full(c, -0.0625, np.float32),
+        "random_pm": lambda r, c: (r.uniform(0.01, 0.2, c) * r.choice([-1, 1], c)).astype(np.float32),
+        "mixed_pow2": lambda r, c: (np.ldexp(1.0, r.integers(-6, -2, c)) * r.choice([-1, 1], c)).astype(np.float32),
+    }[kind]
+    n, L = 2048, 12
+    layers = [_window_layer(rng, n, 32, wfn) for _ in range(L)]
+    bias = np.full(n, 0.05 if kind == "uniform_negative" else -0.1, np.float32)
+    model = NetworkModel(neurons=n, layers=layers, bias=bias)
+    inputs = make_feature_batch(n, (rng.random((n, 2500)) < 0.3).astype(np.float32))
+    prep = engine.prepare_model(model, InferenceConfig(), "optimized")
+    if kind == "uniform_negative":
+        assert all(p.plan.uniform for p in prep)
+    else:
+        assert not any(p.plan.uniform for p in prep)
+    res = engine.infer(model, inputs, InferenceConfig(), prepared=prep)
+    ref = oracle.infer(model, inputs, threads=8)
+    assert np.array_equal(res.categories, ref.categories)
+    assert [o.active_before for o in res.per_layer] + [len(res.categories)] == ref.counts.tolist()
+    assert same_bits(res.final.data, ref.final)
+    assert 0 < len(res.categories) or ref.counts[-1] == 0

@@ -161,3 +161,21 @@ def test_uniform_weight_layers_use_mask_records():
     zero = make_layer_csr(200, np.repeat(np.arange(200), np.diff(layer.row_ptr)),
                           layer.col_idx, vals)
     assert not _check(zero, PlanParams(), rng).uniform
+
+
+def test_default_caps_fit_two_ring_entries_for_every_record_format():
+    """The default caps are tuned for one-word mask records; with per-row
+    weight records (up to 8 words) the planner shrinks them so a block stage
+    still fits half of the kernel's shared memory (two ring entries)."""
+    rng = np.random.default_rng(17)
+    n, k = 2048, 32
+    base = (np.arange(n) * 777) % n
+    cols = ((base[:, None] + np.arange(k)[None, :] * 5) % n).reshape(-1)
+    rows = np.repeat(np.arange(n), k)
+    for vals in (np.full(n * k, 0.0625, np.float32),
+                 (rng.uniform(0.01, 0.2, n * k) * rng.choice([-1, 1], n * k)).astype(np.float32)):
+        plan = build_plans([make_layer_csr(n, rows, cols, vals)], PlanParams())[0]
+        stage = (plan.max_fp_per_stage * 512 + plan.max_records_per_stage * plan.record_words * 4
+                 + plan.max_meta_per_block * 4)
+        assert stage <= 104 * 1024, (plan.record_words, stage)
+        assert plan.rows_per_group == 7
