@@ -93,6 +93,13 @@ def test_layer_dense_multistage_rows(cuda_ok):
     layer = make_layer_csr(n, rows, cols, rng.uniform(-1, 1, 3000).astype(np.float32))
     for p in (PlanParams(rows_per_group=3), PlanParams(rows_per_group=1, reorder=False)):
         _layer_case(layer, p, rng, m=130)
+    # the same pattern with one weight value: mask records, multi-stage blocks
+    # whose extra stages are read from global memory (accumulate_global)
+    uni = make_layer_csr(n, rows, cols, np.full(3000, 0.0625, np.float32))
+    for p in (PlanParams(), PlanParams(rows_per_group=7), PlanParams(rows_per_group=1)):
+        plan = build_plans([uni], p)[0]
+        assert plan.uniform and len(plan.stages) > 0
+        _layer_case(uni, p, rng, m=130)
 
 
 @pytest.mark.parametrize("mode", ["optimized", "baseline"])
