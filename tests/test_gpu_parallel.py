@@ -240,3 +240,37 @@ def test_guard_rewinds_windows(cuda_ok, poison):
                           np.asarray(single.final.data).view(np.uint32))
     ref = oracle.infer(model, inputs)
     assert res.categories.tolist() == ref.categories.tolist()
+
+
+def test_randomized_batch_parallel_matches_single_worker():
+    """Fuzz the in-process batch-parallel runner (2-8 workers, thresholds from
+    1.01 (rebalance at any skew) to 4, skewed densities per shard): the merged
+    result is the single-worker engine's, bit for bit, and the per-layer
+    totals agree."""
+    import os
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    rng = np.random.default_rng(int(os.environ.get("SPDNN_FUZZ_SEED", "99")))
+    for case in range(int(os.environ.get("SPDNN_FUZZ_CASES", "8"))):
+        n = int(rng.choice([256, 1024]))
+        w = int(rng.integers(2, 9))
+        L = int(rng.integers(3, 25))
+        per = int(rng.integers(1, 300))
+        model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+            neurons=n, layers=L, connections_per_neuron=min(n, 32),
+            bias_value=float(rng.uniform(-0.45, -0.2)), seed=int(rng.integers(1 << 30))))
+        dens = rng.uniform(0.15, 0.6, w)
+        x = np.concatenate([(rng.random((n, per)) < d).astype(np.float32) for d in dens], axis=1)
+        inputs = make_feature_batch(n, x)
+        thr = float(rng.choice([1.01, 1.25, 2.0, 4.0]))
+        res, comm, bal = parallel.run_batch_parallel(
+            model, inputs, InferenceConfig(workers=w, rebalance_threshold=thr))
+        single = engine.infer(model, inputs, InferenceConfig())
+        msg = f"case {case}: n={n} w={w} L={L} per={per} thr={thr}"
+        assert np.array_equal(res.categories, single.categories), msg
+        assert [(o.active_before, o.active_after) for o in res.per_layer] == \
+            [(o.active_before, o.active_after) for o in single.per_layer], msg
+        assert np.array_equal(np.asarray(res.final.data).view(np.uint32),
+                              np.asarray(single.final.data).view(np.uint32)), msg
+        assert comm.total_moved == sum(e.moved_rows for e in bal.entries)

@@ -475,3 +475,40 @@ def test_medium_structured_networks_all_record_formats(cuda_ok, kind):
     assert [o.active_before for o in res.per_layer] + [len(res.categories)] == ref.counts.tolist()
     assert same_bits(res.final.data, ref.final)
     assert 0 < len(res.categories) or ref.counts[-1] == 0
+
+
+def test_randomized_structured_networks(cuda_ok):
+    """Fuzz over the generator's family (sizes, fan-in, depth, bias, input
+    density, batch size, one weight value or per-entry weights): categories,
+    per-layer counts and values bit-exact vs the oracle in every case."""
+    rng = np.random.default_rng(int(os.environ.get("SPDNN_FUZZ_SEED", "2026")))
+    for case in range(int(os.environ.get("SPDNN_FUZZ_CASES", "14"))):
+        n = int(rng.choice([97, 257, 1000, 1536, 3000]))
+        k = int(min(n, rng.choice([3, 8, 16, 32, 48])))
+        L = int(rng.integers(2, 16))
+        m = int(rng.integers(1, 2600))
+        bias = float(rng.uniform(-0.6, 0.1))
+        spec = ingest.GeneratorSpec(neurons=n, layers=L, connections_per_neuron=k,
+                                    bias_value=bias, seed=int(rng.integers(1 << 30)))
+        model = ingest.generate_synthetic_network(spec)
+        if case % 3 == 1:  # per-entry weights (weight records, exact form)
+            layers = [make_layer_csr(n, np.repeat(np.arange(n), np.diff(l.row_ptr)), l.col_idx,
+                                     rng.uniform(0.02, 0.12, l.nnz).astype(np.float32))
+                      for l in model.layers]
+            model = NetworkModel(neurons=n, layers=layers, bias=model.bias)
+        elif case % 3 == 2:  # another single weight value (mask records)
+            w = np.float32(rng.choice([0.125, 0.25, -0.0625, 0.1]))
+            layers = [make_layer_csr(n, np.repeat(np.arange(n), np.diff(l.row_ptr)), l.col_idx,
+                                     np.full(l.nnz, w, np.float32)) for l in model.layers]
+            model = NetworkModel(neurons=n, layers=layers, bias=model.bias)
+        x = (rng.random((n, m)) < rng.uniform(0.05, 0.7)).astype(np.float32)
+        if case % 4 == 3:
+            x *= rng.uniform(0.5, 3.0, (n, m)).astype(np.float32)
+        inputs = make_feature_batch(n, x)
+        ref = oracle.infer(model, inputs, threads=8)
+        res = engine.infer(model, inputs, InferenceConfig())
+        msg = f"case {case}: n={n} k={k} L={L} m={m} bias={bias:.3f}"
+        assert np.array_equal(res.categories, ref.categories), msg
+        assert [o.active_before for o in res.per_layer] + [len(res.categories)] == \
+            ref.counts.tolist(), msg
+        assert same_bits(res.final.data, ref.final), msg
