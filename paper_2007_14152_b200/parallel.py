@@ -250,11 +250,15 @@ class DeviceShard:
 
     Layers run in speculative *windows* (see run_layers_parallel): the state
     at the start of a window stays untouched in its buffer (the checkpoint)
-    while the window's layers rotate through the two other buffers, so a
-    window can be rewound and replayed without copying any feature data.
+    while the window's layers rotate through two other buffers, so a window
+    can be rewound and replayed without copying any feature data. A second,
+    speculative window may be enqueued from the first one's (not yet
+    checked) final state while the host waits for the first window's counts;
+    it rotates through the two buffers that are neither checkpoint.
     """
 
-    BUFFERS = 3
+    BUFFERS = 4
+    supports_speculation = True
 
     def __init__(self, net, neurons: int, m_cap: int, num_layers: int, unpadded=None):
         from . import engine
@@ -272,6 +276,7 @@ class DeviceShard:
         self.fma = None  # None: the network's default form; False: exact form
         self.unpadded_active = False
         self._win = None
+        self._spec = None
 
     def load(self, x_rows, categories) -> None:
         """x_rows: (M, N) feature-major host or device tensor. Resets the
@@ -283,21 +288,44 @@ class DeviceShard:
     # -- windows ----------------------------------------------------------
     def begin_window(self, l0: int, k: int) -> None:
         """Enqueue layers l0..l0+k-1 from the current state (no host sync)."""
-        self._win = (l0, k, self.cur, self.m, self.used)
-        self._enqueue(l0, k)
+        self._spec = None
+        self._win = dict(l0=l0, k=k, start=self.cur, m=self.m, used=self.used)
+        self._win["final"] = self._enqueue(l0, k, self.cur, set_m=True, avoid=None)
+        self._win["counts"] = self._snapshot(l0, k)
 
-    def _enqueue(self, l0: int, k: int) -> None:
+    def begin_speculative(self, l0: int, k: int) -> None:
+        """Enqueue layers l0..l0+k-1 from the current window's final state
+        before its counts are known (they are produced on the device)."""
+        w = self._win
+        spec = dict(l0=l0, k=k, start=w["final"])
+        spec["final"] = self._enqueue(l0, k, w["final"], set_m=False, avoid=w["start"])
+        spec["counts"] = self._snapshot(l0, k)
+        self._spec = spec
+
+    def drop_speculative(self) -> None:
+        """Forget the speculative window (later work overwrites its buffers)."""
+        self._spec = None
+
+    def promote_speculative(self) -> None:
+        """After commit(): the speculative window, started from the committed
+        state, becomes the current window."""
+        spec = self._spec
+        assert spec is not None and spec["start"] == self.cur
+        spec.update(m=self.m, used=self.used)
+        self._win, self._spec = spec, None
+
+    def _enqueue(self, l0: int, k: int, ck: int, set_m: bool, avoid) -> int:
         import ctypes
         from . import _native
         e, ws, net = self.engine, self.ws, self.net
-        ck = self.cur
-        ws.counts[l0] = self.m
+        if set_m:
+            ws.counts[l0] = self.m
         ws.counts[l0 + 1: l0 + k + 1].zero_()
         ws.work[l0: l0 + k].zero_()
         opts = e.run_opts(net, self.fma)
         stream = e._stream_ptr(e._torch())
         cnt = ws.counts.data_ptr()
-        o1, o2 = (ck + 1) % 3, (ck + 2) % 3
+        o1, o2 = [b for b in range(self.BUFFERS) if b != ck and b != avoid][:2]
         _native.check(_native.lib().spdnn_layer_forward(
             ctypes.byref(net.layer_devs[l0]), e._dptr(net.bias), e._dptr(ws.y[ck]),
             e._dptr(ws.y[o1]), ws.ld, e._dptr(ws.a[ck]), e._dptr(ws.cat[ck]),
@@ -316,30 +344,42 @@ class DeviceShard:
                 e._dptr(ws.a[o1]), e._dptr(ws.a[o2]), e._dptr(ws.cat[o1]), e._dptr(ws.cat[o2]),
                 ctypes.c_void_p(cnt + 4 * (l0 + 1)), ctypes.byref(sc), ctypes.byref(opts),
                 stream), "spdnn_infer_layers")
-        self._final = o1 if (k - 1) % 2 == 0 else o2
+        return o1 if (k - 1) % 2 == 0 else o2
+
+    def _snapshot(self, l0: int, k: int):
+        """The window's counts and the guard word, copied on the stream right
+        after its last layer (a later speculative window cannot leak in), and
+        an event the transport waits on instead of the whole stream."""
+        torch = self.engine._torch()
+        t = torch.cat([self.ws.counts[l0 + 1: l0 + k + 1], self.ws.guard]).to(torch.int64)
+        ev = torch.cuda.Event()
+        ev.record()
+        return t, ev
 
     def window_counts(self):
         """Device int64 [active after each window layer..., guard bits]."""
-        torch = self.engine._torch()
-        l0, k = self._win[0], self._win[1]
-        return torch.cat([self.ws.counts[l0 + 1: l0 + k + 1], self.ws.guard]).to(torch.int64)
+        return self._win["counts"][0]
+
+    def window_event(self):
+        return self._win["counts"][1]
 
     def rewind(self) -> None:
         """Back to the window's starting state (its buffer was never written)."""
-        self.cur, self.m, self.used = self._win[2], self._win[3], self._win[4]
+        w = self._win
+        self._spec = None
+        self.cur, self.m, self.used = w["start"], w["m"], w["used"]
 
     def replay(self, k: int) -> None:
         """Rewind and run only the first k layers of the window."""
-        l0 = self._win[0]
+        l0 = self._win["l0"]
         self.rewind()
-        self._win = (l0, k) + self._win[2:]
-        self._enqueue(l0, k)
+        self.begin_window(l0, k)
 
     def commit(self, m_last_in: int, m: int) -> None:
         """Accept the window: its last output becomes the current state. The
         kernel writes a feature's outputs at its input position, so the
         columns in use are those of the last layer's input."""
-        self.cur = self._final
+        self.cur = self._win["final"]
         self.m, self.used = int(m), int(m_last_in)
         self._win = None
 
@@ -418,6 +458,24 @@ class DeviceShard:
 # ---------------------------------------------------------------------------
 # transports
 
+_SIDE = {}
+
+
+def _side_stream(torch):
+    """A per-device side stream for the window count reads."""
+    dev = torch.cuda.current_device()
+    if dev not in _SIDE:
+        _SIDE[dev] = torch.cuda.Stream()
+    return _SIDE[dev]
+
+
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
 class LocalTransport:
     """All workers in this process (the reference's threads; one GPU)."""
 
@@ -435,10 +493,18 @@ class LocalTransport:
                         self.hook(CountMsg(src=w, layer=layer, count=mine[w]))
         return [mine[w] for w in range(self.workers)]
 
-    def allgather_window(self, mine: dict) -> np.ndarray:
-        """(workers, k+1) host array of every worker's window counts + guard."""
+    def allgather_window(self, mine: dict, events: dict | None = None) -> np.ndarray:
+        """(workers, k+1) host array of every worker's window counts + guard.
+        With `events`, the copy waits for those only (on a side stream), not
+        for a speculative window enqueued after them."""
         import torch
-        return torch.stack([mine[w] for w in range(self.workers)]).cpu().numpy()
+        if not events:
+            return torch.stack([mine[w] for w in range(self.workers)]).cpu().numpy()
+        side = _side_stream(torch)
+        for ev in events.values():
+            side.wait_event(ev)
+        with torch.cuda.stream(side):
+            return torch.stack([mine[w] for w in range(self.workers)]).cpu().numpy()
 
     def exchange(self, layer: int, plan: TransferPlan, shards: dict) -> None:
         incoming = {w: [] for w in range(self.workers)}
@@ -497,14 +563,23 @@ class DistTransport:
                     self.hook(CountMsg(src=self.rank, layer=layer, count=mine[self.rank]))
         return [int(v.item()) for v in out]
 
-    def allgather_window(self, mine: dict) -> np.ndarray:
+    def allgather_window(self, mine: dict, events: dict | None = None) -> np.ndarray:
         """One allgather of the window's counts (device-resident under NCCL)
-        and one host read for the whole window."""
+        and one host read for the whole window. With `events` it runs on a
+        side stream that waits for this rank's window only, so a speculative
+        window already enqueued keeps the GPU busy meanwhile."""
         import torch
-        t = self._wire(mine[self.rank].contiguous())
-        out = [self._empty(t.shape[0], torch.int64) for _ in range(self.workers)]
-        self.dist.all_gather(out, t)
-        return torch.stack(out).cpu().numpy()
+        ctx = None
+        if events:
+            side = _side_stream(torch)
+            for ev in events.values():
+                side.wait_event(ev)
+            ctx = torch.cuda.stream(side)
+        with (ctx if ctx is not None else _nullcontext()):
+            t = self._wire(mine[self.rank].contiguous())
+            out = [self._empty(t.shape[0], torch.int64) for _ in range(self.workers)]
+            self.dist.all_gather(out, t)
+            return torch.stack(out).cpu().numpy()
 
     def exchange(self, layer: int, plan: TransferPlan, shards: dict) -> None:
         import torch
@@ -555,6 +630,8 @@ class DistTransport:
 
 WINDOW_MIN = 4
 WINDOW_MAX = int(__import__("os").environ.get("SPDNN_WINDOW_MAX", "64"))
+# enqueue the next window before reading this one's counts (DeviceShard)
+SPECULATE = __import__("os").environ.get("SPDNN_SPECULATE", "1") == "1"
 
 
 def run_layers_parallel(num_layers: int, shards: dict, transport, threshold: float,
@@ -587,15 +664,32 @@ def run_layers_parallel(num_layers: int, shards: dict, transport, threshold: flo
     before = sum(transport.allgather_counts(-1, {w: shards[w].m for w in local}))
     k_max = max(1, window or WINDOW_MAX)
     k_cur = min(WINDOW_MIN, k_max)
+    speculate = SPECULATE and all(getattr(shards[w], "supports_speculation", False)
+                                  for w in local)
+    current = False  # a window (the promoted speculation) is already enqueued
+    k = 0
     l = 0
     while l < num_layers:
         if before == 0:
+            if current:
+                for w in local:
+                    shards[w].drop_speculative()
             totals.extend([(0, 0)] * (num_layers - l))
             break
-        k = min(k_cur, num_layers - l)
-        for w in local:
-            shards[w].begin_window(l, k)
-        hist = transport.allgather_window({w: shards[w].window_counts() for w in local})
+        if not current:
+            k = min(k_cur, num_layers - l)
+            for w in local:
+                shards[w].begin_window(l, k)
+        current = False
+        # the next window, enqueued from this one's unchecked final state: it
+        # keeps the GPU busy while the host waits for this window's counts
+        nk = min(2 * k_cur, k_max, num_layers - l - k) if speculate else 0
+        if nk > 0:
+            for w in local:
+                shards[w].begin_speculative(l + k, nk)
+        events = {w: shards[w].window_event() for w in local} if speculate else None
+        hist = transport.allgather_window({w: shards[w].window_counts() for w in local},
+                                          events)
         guard = int(np.bitwise_or.reduce(hist[:, k]))
         unpadded = bool(guard & 2)
         if (guard & 1 and any(shards[w].uses_fma for w in local)) or \
@@ -615,7 +709,7 @@ def run_layers_parallel(num_layers: int, shards: dict, transport, threshold: flo
                 break
         if accept < k:
             for w in local:
-                shards[w].replay(accept)
+                shards[w].replay(accept)  # drops the speculative window
         for j in range(accept):
             counts = [int(c) for c in hist[:, j]]
             if hook is not None:
@@ -643,10 +737,20 @@ def run_layers_parallel(num_layers: int, shards: dict, transport, threshold: flo
             shards[w].commit(last_in, int(hist[w, accept - 1]))
         l += accept
         if plan:
+            if nk > 0:
+                for w in local:
+                    shards[w].drop_speculative()
             transport.exchange(l - 1, plan, shards)
             k_cur = min(WINDOW_MIN, k_max)
         else:
             k_cur = min(2 * k_cur, k_max)
+            if nk > 0 and accept == k and sum(int(c) for c in hist[:, k - 1]) > 0:
+                for w in local:
+                    shards[w].promote_speculative()
+                current, k = True, nk
+            elif nk > 0:
+                for w in local:
+                    shards[w].drop_speculative()
     parts = transport.gather(shards, values)
     return totals, comm, balance, parts
 
