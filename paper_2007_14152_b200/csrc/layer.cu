@@ -234,6 +234,7 @@ struct LayerArgs {
   uint32_t mentry_bytes;
   int simple_wait;     // 1: consumer warps visit every (C/gpi)-th entry and (C/gpi) | nbuf
   int gpi;             // consumer work units (row groups) per item = max groups per block
+  uint32_t act_off;    // activity bytes: [nbuf][gpi][32 lanes], one byte per lane and unit
 };
 
 // Ring-buffer header written by the producer (one per buffer fill).
@@ -529,7 +530,7 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
 template <int R, bool FMA, int FPL>
 __device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int *rows,
                                          const float *bias, int t, int lane, int M,
-                                         uint32_t *s_alive) {
+                                         uint8_t *act) {
   constexpr int T = Geo<FPL>::kTileF;
   const int j0 = t * T + FPL * lane;
   const int valid = M - j0;  // features of this lane that exist (may be <= 0)
@@ -538,12 +539,9 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int
                           ? finish_rows<R, FMA, FPL, true>(A, acc, rows, bias, j0, valid, tiny)
                           : finish_rows<R, FMA, FPL, false>(A, acc, rows, bias, j0, valid, tiny);
   if (FMA && tiny) atomicOr(A.guard, 1u);
-  // activity masks, q-major: word q bit l <=> feature FPL*l + q of the tile
-#pragma unroll
-  for (int q = 0; q < FPL; q++) {
-    const uint32_t word = __ballot_sync(0xffffffffu, (am >> q) & 1u);
-    if (lane == 0 && word) atomicOr(&s_alive[q], word);
-  }
+  // the lane's activity bits (bit q <=> feature FPL*lane + q is > 0), one
+  // plain byte store: the publisher warp ORs the item's units together
+  act[lane] = (uint8_t)am;
 }
 
 // Extra stages of a lone oversized group (rare: a row group whose inputs
@@ -603,7 +601,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs], s_free[kMaxBufs];
-  __shared__ uint32_t s_alive[kMaxBufs][4];
   __shared__ float s_wmask;
 #ifdef SPDNN_PROFILE
   __shared__ long long s_tgr[kMaxBufs], s_tpost[kMaxBufs], s_tempty[kMaxBufs];
@@ -640,7 +637,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
       mbar_init(empty0 + 8 * i, gpi);  // one arrival per work unit (row group) of the item
       mbar_init(free0 + 8 * i, 1);     // the publisher's release of the slot
-      for (int w = 0; w < 4; w++) s_alive[i][w] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -935,9 +931,18 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         s_tempty[slot] = now;
       }
 #endif
-      uint32_t wv = lane < FPL ? s_alive[slot][lane] : 0u;
-      if (lane < FPL) s_alive[slot][lane] = 0u;
-      __syncwarp();
+      // OR the units' activity bytes (this lane's FPL features), then turn
+      // them into the tile's q-major words (word q bit l <=> feature FPL*l+q)
+      const int ng = reinterpret_cast<const volatile Header *>(smem + slot * A.buf_bytes)->ng;
+      const uint8_t *act = reinterpret_cast<const uint8_t *>(smem + A.act_off) + slot * gpi * 32;
+      uint32_t am = 0u;
+      for (int g = 0; g < ng; g++) am |= act[g * 32 + lane];
+      uint32_t wv = 0u;
+#pragma unroll
+      for (int q = 0; q < FPL; q++) {
+        const uint32_t word = __ballot_sync(0xffffffffu, (am >> q) & 1u);
+        if (lane == q) wv = word;
+      }
       if (lane == 0) mbar_arrive(free0 + 8 * slot);
       if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * t + lane], wv);
       __syncwarp();
@@ -1055,12 +1060,13 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         rows[r] = mrows[r];
         bias[r] = mbias[r];
       }
-      epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M, s_alive[slot]);
+      epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M,
+                            reinterpret_cast<uint8_t *>(smem + A.act_off) + (slot * gpi + g) * 32);
       PROF_MARK(2);  // [2] epilogue
     }
-    // the unit's activity bits went to s_alive[slot] (lane 0's shared
-    // atomics, ordered before its arrival by the mbarrier's release); the
-    // publisher warp folds them into the tile once every unit has arrived
+    // the unit's activity bytes (every lane's store, ordered before lane 0's
+    // arrival by __syncwarp and the mbarrier's release) are folded into the
+    // tile by the publisher warp once every unit has arrived
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * slot);
     g += C;
@@ -1151,13 +1157,16 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   const size_t mentry = ((8 + G::kTileF + fpcap) * 4 + 15) / 16 * 16;
   const size_t mring = (size_t)kMetaRing * mentry;
   const size_t budget = optin - 2048 - mring;  // static shared memory + reserve
-  const int nbuf = (int)std::min<size_t>(kMaxBufs, budget / buf);
+  // + the per-unit activity bytes of each entry (gpi <= max(groups, C))
+  const size_t act_unit = 32, act_max = (size_t)std::max(L.max_groups_per_block, G::kC) * act_unit;
+  const int nbuf = (int)std::min<size_t>(kMaxBufs, budget / (buf + act_max));
   if (nbuf < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
   // units per item: at least the block's groups, and enough that a consumer
   // warp's consecutive units are at most nbuf ring entries apart
   const int gpi = std::max(std::max(1, L.max_groups_per_block), (G::kC + nbuf - 1) / nbuf);
-  const size_t smem = (size_t)nbuf * buf + mring;
+  const size_t smem = (size_t)nbuf * buf + mring + (size_t)nbuf * gpi * act_unit;
   A.mring_off = (uint32_t)(nbuf * buf);
+  A.act_off = (uint32_t)(nbuf * buf + mring);
   A.mentry_bytes = (uint32_t)mentry;
   A.meta_bytes = (uint32_t)meta;
   A.rec_bytes = (uint32_t)rec;
