@@ -157,6 +157,44 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_cp_async_arrive_inc(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
+// ---- cross-layer readiness (LayerArgs::xl) ----------------------------------
+constexpr uint32_t kBig = 1u << 30;  // completion counter target (see publisher)
+__device__ __forceinline__ int ld_relaxed(const int32_t *p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel() {
+#ifndef SPDNN_XL_NO_ACQ_FENCE
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void fence_proxy_async() {
+#ifndef SPDNN_XL_NO_PROXY_FENCE
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void st_release_u(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t atom_add_acq_rel_u(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
+               : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_u(uint32_t *p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_release(int32_t *p, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // TMA tile gather: rows r0..r3 of the 2-D tensor, columns [col, col + box),
 // into 4 consecutive smem rows; completion as tx bytes on `bar`
 __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap *tmap, int col,
@@ -235,6 +273,17 @@ struct LayerArgs {
   int simple_wait;     // 1: consumer warps visit every (C/gpi)-th entry and (C/gpi) | nbuf
   int gpi;             // consumer work units (row groups) per item = max groups per block
   uint32_t act_off;    // activity bytes: [nbuf][gpi][32 lanes], one byte per lane and unit
+  // Cross-layer mode (xl = 1, spdnn_infer_layers with the scratch's xl buffers):
+  // no griddepcontrol.wait -- an item's input tile is used as soon as it is
+  // published. ready_in[t] counts the survivors the previous layer appended
+  // to positions [T t, T t + T); *cnt_in == kBig once m_in is final and every
+  // append is done. This layer publishes the same for the next one.
+  int xl;
+  const int32_t *ready_in;  // null for the first layer (its input is final)
+  int32_t *ready_out;
+  const uint32_t *cnt_in;  // the previous layer's cnt_out (kBig from the start: first layer)
+  uint32_t *cnt_out;  // completed tiles + (kBig - tiles) once the tile total is known
+  uint32_t *added;    // CAS flag: the tile total was added to cnt_out
 };
 
 // Ring-buffer header written by the producer (one per buffer fill).
@@ -242,7 +291,7 @@ struct Header {
   int item;     // -1: no more work
   int entry;    // ring entry number (stale-phase check)
   int t, b;
-  int nst;
+  int nst;      // cross-layer mode: | features of the tile that exist (1..T) << 16
   int ng;
   int rec_cnt;  // records of this stage (multi-stage: all belong to group 0)
   int fp_cnt;
@@ -596,7 +645,9 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
   }
 }
 
-template <int R, bool FMA, int FPL, bool MASK>
+// XL: cross-layer mode (LayerArgs::xl), a separate instantiation so that the
+// classic kernel carries none of its code
+template <int R, bool FMA, int FPL, bool MASK, bool XL>
 __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
@@ -607,6 +658,8 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   __shared__ unsigned long long s_tfirst[kMaxBufs];
 #endif
   __shared__ int s_items[8];  // producer: item index of ring entry j (j & 7)
+  __shared__ int s_valid[8];  // producer, cross-layer mode: features of entry j's tile, -1 = none
+  __shared__ int s_mfin;      // producer, cross-layer mode: final input count once seen, else -1
 
   using G = Geo<FPL, MASK>;
   constexpr int RW = MASK ? 1 : Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
@@ -633,6 +686,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
 
   if (tid == 0) {
     s_wmask = __uint_as_float(A.L.weight_bits);
+    s_mfin = -1;
     for (int i = 0; i < nbuf; i++) {
       mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
       mbar_init(empty0 + 8 * i, gpi);  // one arrival per work unit (row group) of the item
@@ -641,7 +695,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (warp < C || warp >= C + P) {
+  if (!XL && (warp < C || warp >= C + P)) {
     dep_wait();
     if (M <= 0) return;
   }
@@ -723,6 +777,67 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     pbar();
     for (int j = 0; j < kFpAhead; j++) prefetch_fp(j);
     cp_async_commit();
+    // Cross-layer mode: one producer thread (the resolver, which has no copy
+    // duties) decides for each claimed item whether its input tile exists
+    // and has been published, polling the previous layer's counters. Its
+    // relaxed read of the next item's counter is issued one iteration early
+    // so that the steady state pays no round trip; a fence turns the read
+    // into an acquire, the producers' named barrier carries it to the other
+    // threads and fence.proxy.async to their TMA reads of the rows.
+    const int kRes = P * 32 - 1;
+    int m_fin = -1;   // resolver: the layer's final input count, once seen
+    int pre = -1;     // resolver: early read of the next item's ready counter
+    auto resolve = [&](int t, int pre_v) -> int {
+      if (m_fin < 0 && pre_v >= T) {
+        fence_acq_rel();
+        return T;
+      }
+      for (uint32_t spin = 0;; spin++) {
+        if (m_fin >= 0) return t * T < m_fin ? min(T, m_fin - t * T) : -1;
+        if (A.ready_in && (int64_t)(t + 1) * T <= A.ld && ld_relaxed(A.ready_in + t) >= T) {
+          fence_acq_rel();
+          return T;
+        }
+        if (ld_relaxed_u(A.cnt_in) == kBig) {
+          fence_acq_rel();
+          m_fin = *reinterpret_cast<const volatile int32_t *>(A.m_in);
+          // the tile total joins this layer's completion counter exactly once
+          if (atomicCAS(A.added, 0u, 1u) == 0u) {
+            const uint32_t tl = (uint32_t)((m_fin + T - 1) / T);
+            red_add_u(A.cnt_out, kBig - tl);
+          }
+          continue;
+        }
+        __nanosleep(256);
+        if (spin > (1u << 26)) __trap();  // the previous layer never published
+      }
+    };
+    auto preload = [&](int j) {  // resolver: early relaxed read for entry j
+      const int t = item_of(j) / nb;
+      pre = (m_fin < 0 && A.ready_in && (int64_t)(t + 1) * T <= A.ld) ? ld_relaxed(A.ready_in + t)
+                                                                      : -1;
+    };
+    // once the input is final (the previous layer completed) every thread
+    // derives validity from the count itself: no polls, fences or barrier
+    int mf = -1;
+    if (XL) {
+      if (ptid == kRes) {
+        for (int j = 0; j < kMetaAhead; j++) s_valid[j] = resolve(item_of(j) / nb, -1);
+        preload(kMetaAhead);
+        if (m_fin >= 0) s_mfin = m_fin;
+      }
+      pbar();
+      mf = s_mfin;
+      fence_proxy_async();
+      for (int j = 0; j < kMetaAhead; j++) {
+        if (s_valid[j] <= 0) continue;
+        const int t0 = item_of(j) / nb;
+        const uint32_t e = (uint32_t)__cvta_generic_to_shared(ment(j));
+        if (ptid >= 2 && ptid < 2 + T / 4)
+          cp_async16(e + 32 + 16 * (ptid - 2), A.a_in + t0 * T + 4 * (ptid - 2));
+      }
+      cp_async_commit();
+    } else {
     // the feature columns of the first entries are fetched together with
     // the active count (one round trip): the tile of a statically dealt item
     // is known without M, and a tile inside the a_in allocation is safe to
@@ -742,6 +857,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       cp_async_wait<0>();
       return;
     }
+    }  // classic prologue
     cp_async_wait<0>();
     pbar();
     for (int k = 0;; k++) {
@@ -756,7 +872,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       cp_async_wait<1>();
       pbar();
       const int item = item_of(k);
-      if (item >= items) {
+      if (XL ? s_valid[k & 7] < 0 : item >= items) {
         cp_async_wait<0>();
         if (pw == 0) {
           // end markers in the next nbuf entries; a consumer warp waits at most
@@ -782,7 +898,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const int *ain = en + 8;
       const int *sfp = en + 8 + T;
       // feature columns 32q + lane (q < FPL) of tile t
-      const int valid = min(T, M - t * T);
+      const int valid = XL ? s_valid[k & 7] : min(T, M - t * T);
       int src[FPL];
 #pragma unroll
       for (int q = 0; q < FPL; q++) src[q] = 32 * q + lane < valid ? ain[32 * q + lane] : -1;
@@ -847,6 +963,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         h->ng = ng;
         h->rec_cnt = rec_cnt;
         h->fp_cnt = fp_cnt;
+        if (XL) h->nst = nst | (valid << 16);
 #ifdef SPDNN_PROFILE
         s_tpost[slot] = clock64();
 #endif
@@ -895,7 +1012,25 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       // (staged rows; its descriptor landed with this iteration's wait):
       // ring entry k's slot is reused by k + kMetaRing > k + kMetaAhead only.
       // Issued after the header went out: off the slot turnaround path.
-      prefetch_desc(k + kMetaAhead, true, true);
+      int v_ahead = 1;
+      if (XL) {
+        if (mf < 0) {  // uniform: every producer thread updates mf after the same barrier
+          if (ptid == kRes) {
+            s_valid[(k + kMetaAhead) & 7] = resolve(item_of(k + kMetaAhead) / nb, pre);
+            preload(k + kMetaAhead + 1);  // claimed at the top of this iteration
+            if (m_fin >= 0) s_mfin = m_fin;
+          }
+          pbar();
+          mf = s_mfin;
+          fence_proxy_async();
+          v_ahead = s_valid[(k + kMetaAhead) & 7];
+        } else {
+          const int ta = item_of(k + kMetaAhead) / nb;
+          v_ahead = ta * T < mf ? min(T, mf - ta * T) : -1;
+          if (ptid == kRes) s_valid[(k + kMetaAhead) & 7] = v_ahead;
+        }
+      }
+      prefetch_desc(k + kMetaAhead, true, v_ahead > 0);
       prefetch_fp(k + kFpAhead);
       cp_async_commit();
       PROF_MARK(5);  // [5] header
@@ -912,6 +1047,26 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     // the bits into the tile's word, count the tile's finished blocks, and
     // the item that completes tile t appends the tile's survivors to
     // a_out / cat_out (pruning without a pass over Y).
+    // Cross-layer mode: a finished tile's survivors are announced to the next
+    // layer (per next-layer tile) and the tile counted complete once the
+    // stores are fenced -- done one entry later, after that entry's slot has
+    // gone back to the producer, so the fence never delays a slot release.
+    // The counter reaching kBig is the next layer's "input final".
+    int pend_base = 0, pend_tot = -1;
+    auto publish = [&]() {
+      if (!XL || pend_tot < 0) return;
+      fence_acq_rel();  // every lane: its a_out / cat_out stores first
+      __syncwarp();
+      if (lane == 0) {
+        for (int p = pend_base, e = pend_base + pend_tot; p < e;) {
+          const int tt = p / T, n = min(e, (tt + 1) * T) - p;
+          red_add_release(A.ready_out + tt, n);
+          p += n;
+        }
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.cnt_out) : "memory");
+      }
+      pend_tot = -1;
+    };
     for (int k = 0;; k++) {
       const int slot = k % nbuf;
       const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
@@ -944,6 +1099,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         if (lane == q) wv = word;
       }
       if (lane == 0) mbar_arrive(free0 + 8 * slot);
+      publish();  // the previous entry's tile, if it completed one
       if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * t + lane], wv);
       __syncwarp();
       int last = 0;
@@ -959,11 +1115,16 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        if (lane < FPL) {
-          wv = atomicOr(&A.tile_alive[FPL * t + lane], 0u);
-          A.tile_alive[FPL * t + lane] = 0u;
+        if (XL) {  // reset with atomics: the set is reused two launches later
+          if (lane < FPL) wv = atomicExch(&A.tile_alive[FPL * t + lane], 0u);
+          if (lane == 0) atomicExch(&A.tile_done[t], 0);
+        } else {
+          if (lane < FPL) {
+            wv = atomicOr(&A.tile_alive[FPL * t + lane], 0u);
+            A.tile_alive[FPL * t + lane] = 0u;
+          }
+          if (lane == 0) A.tile_done[t] = 0;
         }
-        if (lane == 0) A.tile_done[t] = 0;
         uint32_t mw[FPL];
         int tot = 0, below = 0;
 #pragma unroll
@@ -982,12 +1143,18 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
           if ((mw[q] >> lane) & 1u) {
             const int j = t * T + FPL * lane + q;
             A.a_out[rank] = j;
-            A.cat_out[rank] = A.cat_in[j];
+            // (cross-layer: written by another SM's publisher, read past L1)
+            A.cat_out[rank] = XL ? __ldcg(A.cat_in + j) : A.cat_in[j];
             rank++;
           }
         }
+        if (XL) {  // signalled after the next slot release (publish below)
+          pend_base = base;
+          pend_tot = tot;
+        }
       }
     }
+    publish();
     return;
   }
 
@@ -1046,7 +1213,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         accumulate<R, FMA, FPL, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
                                    meta[seg_base + 2 * g + 1], ybase, negz2);
       }
-      if (h.nst > 1) accumulate_global<R, FMA, FPL, MASK>(A, acc, h.b, h.t, lane, M, negz2);
+      // the features of the tile that exist end at Mt
+      const int Mt = XL ? h.t * T + (h.nst >> 16) : M;
+      if ((XL ? (h.nst & 0xffff) : h.nst) > 1)
+        accumulate_global<R, FMA, FPL, MASK>(A, acc, h.b, h.t, lane, Mt, negz2);
       PROF_MARK(1);  // [1] record loop
       // output rows and their biases (staged with the block metadata) are read
       // only now, so they hold no registers across the record loop
@@ -1060,7 +1230,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         rows[r] = mrows[r];
         bias[r] = mbias[r];
       }
-      epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M,
+      epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, Mt,
                             reinterpret_cast<uint8_t *>(smem + A.act_off) + (slot * gpi + g) * 32);
       PROF_MARK(2);  // [2] epilogue
     }
@@ -1085,21 +1255,28 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
 
 // ---- launch configuration ---------------------------------------------------
 
-template <int R, int FPL, bool MASK>
+template <int R, int FPL, bool MASK, bool XL>
 void *kernel_ptr(bool fma) {
-  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true, FPL, MASK>)
-             : reinterpret_cast<void *>(&layer_kernel<R, false, FPL, MASK>);
+  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true, FPL, MASK, XL>)
+             : reinterpret_cast<void *>(&layer_kernel<R, false, FPL, MASK, XL>);
 }
 
-template <int FPL, bool MASK>
-void *kernel_for(int R, bool fma) {
+template <int FPL, bool MASK, bool XL>
+void *kernel_for_xl(int R, bool fma) {
   switch (R) {
-    case 1: return kernel_ptr<1, FPL, MASK>(fma);
-    case 3: return kernel_ptr<3, FPL, MASK>(fma);
-    case 6: return kernel_ptr<6, FPL, MASK>(fma);
-    case 7: return kernel_ptr<7, FPL, MASK>(fma);
+    case 1: return kernel_ptr<1, FPL, MASK, XL>(fma);
+    case 3: return kernel_ptr<3, FPL, MASK, XL>(fma);
+    case 6: return kernel_ptr<6, FPL, MASK, XL>(fma);
+    case 7: return kernel_ptr<7, FPL, MASK, XL>(fma);
     default: return nullptr;
   }
+}
+
+// the cross-layer instantiations exist for 128-feature items (FPL = 4) only
+template <int FPL, bool MASK>
+void *kernel_for(int R, bool fma, bool xl) {
+  if (FPL == 4 && xl) return kernel_for_xl<4, MASK, true>(R, fma);
+  return kernel_for_xl<FPL, MASK, false>(R, fma);
 }
 
 struct DevInfo {
@@ -1137,10 +1314,10 @@ int device_info(int &sms, size_t &optin) {
 }
 
 template <int FPL, bool MASK>
-int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
+int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   using G = Geo<FPL, MASK>;
   const spdnn_layer_dev &L = A.L;
-  void *fn = kernel_for<FPL, MASK>(L.rows_per_group, fma);
+  void *fn = kernel_for<FPL, MASK>(L.rows_per_group, fma, A.xl != 0);
   if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1, 3, 6 or 7");
   if (MASK != (L.uniform != 0) || (MASK && L.record_words != 1))
     return spdnn_fail(SPDNN_EINVAL, "layer: record format does not match the layout");
@@ -1209,7 +1386,7 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream) {
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = kUsePdl;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   e = cudaLaunchKernelExC(&cfg, fn, args);
@@ -1323,10 +1500,22 @@ int tensor_map_for(const float *y, int64_t n, int64_t ld, int box_cols, CUtensor
   return rc;
 }
 
+// Cross-layer links of one launch (infer_layers with the scratch's xl buffers).
+struct XlLink {
+  int32_t *tile_done;
+  uint32_t *tile_alive;
+  const int32_t *ready_in;
+  int32_t *ready_out;
+  const uint32_t *cnt_in;
+  uint32_t *cnt_out, *added;
+  bool pdl;
+};
+
 int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, float *y_out,
             int64_t ld, const int32_t *a_in, const int64_t *cat_in, const int32_t *m_in,
             int32_t *a_out, int64_t *cat_out, int32_t *m_out, const spdnn_scratch *scratch,
-            int32_t *work, const spdnn_run_opts *opts, void *stream) {
+            int32_t *work, const spdnn_run_opts *opts, void *stream,
+            const XlLink *xl = nullptr) {
   // ld * 4 must fit 32 bits: the epilogue forms row addresses with one wide multiply
   if (!layer || !bias || !y_in || !y_out || !a_in || !cat_in || !m_in || !a_out ||
       !cat_out || !m_out || !scratch || !work || ld < 1 || ld % SPDNN_TILE_FEATURES ||
@@ -1361,10 +1550,23 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   std::memcpy(&tb, &A.tiny, 4);
   A.tiny_bits_m1 = tb ? tb - 1u : 0u;
   A.negz = -0.0f;
+  bool pdl = kUsePdl != 0;
+  if (xl) {
+    A.xl = 1;
+    A.tile_done = xl->tile_done;
+    A.tile_alive = xl->tile_alive;
+    A.ready_in = xl->ready_in;
+    A.ready_out = xl->ready_out;
+    A.cnt_in = xl->cnt_in;
+    A.cnt_out = xl->cnt_out;
+    A.added = xl->added;
+    pdl = xl->pdl;
+  }
   const bool mask = layer->uniform != 0;
   cudaStream_t st = (cudaStream_t)stream;
-  if (fpl == 2) return mask ? launch_layer<2, true>(A, fma, st) : launch_layer<2, false>(A, fma, st);
-  return mask ? launch_layer<4, true>(A, fma, st) : launch_layer<4, false>(A, fma, st);
+  if (fpl == 2)
+    return mask ? launch_layer<2, true>(A, fma, st, pdl) : launch_layer<2, false>(A, fma, st, pdl);
+  return mask ? launch_layer<4, true>(A, fma, st, pdl) : launch_layer<4, false>(A, fma, st, pdl);
 }
 
 }  // namespace
@@ -1386,15 +1588,40 @@ static int infer_layers(int64_t num_layers, const spdnn_layer_dev *layers, const
                         void *const *events) {
   if (num_layers < 0 || (num_layers > 0 && (!layers || !scratch)))
     return spdnn_fail(SPDNN_EINVAL, "spdnn_infer_layers: bad argument");
-  float *y[2] = {y0, y1};
-  int32_t *a[2] = {a0, a1};
-  int64_t *cat[2] = {cat0, cat1};
+  // cross-layer mode: every layer launches (no empty layout) and all the
+  // optional buffers are there
+  bool xl = scratch->y2 && scratch->a2 && scratch->cat2 && scratch->tile_done2 &&
+            scratch->tile_alive2 && scratch->ready && scratch->sync;
+  for (int64_t l = 0; xl && l < num_layers; l++) xl = layers[l].num_blocks > 0;
+  if (opts && opts->features_per_lane == 2) xl = false;  // no FPL = 2 instantiation
+  float *y[3] = {y0, y1, scratch->y2};
+  int32_t *a[3] = {a0, a1, scratch->a2};
+  int64_t *cat[3] = {cat0, cat1, scratch->cat2};
+  const int64_t tc = ld / 64;  // ready counters per layer (64-feature tiles at most)
   for (int64_t l = 0; l < num_layers; l++) {
-    int i = (int)(l & 1), o = i ^ 1;
+    const int nbufs = xl ? 3 : 2;
+    const int i = (int)(l % nbufs), o = (int)((l + 1) % nbufs);
     if (events && cudaEventRecord((cudaEvent_t)events[l], (cudaStream_t)stream) != cudaSuccess)
       return spdnn_fail(SPDNN_ECUDA, "spdnn_infer_layers_timed: event record failed");
+    XlLink link;
+    if (xl) {
+      // the first layer waits for everything before it (stream order, no
+      // PDL); later ones only for the tiles they read. At most two layers
+      // are resident (every CTA fills an SM), so two tile sets alternate.
+      link.tile_done = (l & 1) ? scratch->tile_done2 : scratch->tile_done;
+      link.tile_alive = (l & 1) ? scratch->tile_alive2 : scratch->tile_alive;
+      link.ready_in = l ? scratch->ready + l * tc : nullptr;
+      link.ready_out = scratch->ready + (l + 1) * tc;
+      // sync = [cnt_0 .. cnt_L][added_0 .. added_L]: cnt_0 = kBig (set by the
+      // caller: the first layer's input is final), cnt_{l+1} = layer l's
+      link.cnt_in = scratch->sync + l;
+      link.cnt_out = scratch->sync + l + 1;
+      link.added = scratch->sync + (num_layers + 1) + l;
+      link.pdl = l > 0;
+    }
     int rc = forward(&layers[l], bias, y[i], y[o], ld, a[i], cat[i], counts + l, a[o], cat[o],
-                     counts + l + 1, scratch, scratch->work + l, opts, stream);
+                     counts + l + 1, scratch, scratch->work + l, opts, stream,
+                     xl ? &link : nullptr);
     if (rc) return rc;
   }
   if (events && cudaEventRecord((cudaEvent_t)events[num_layers], (cudaStream_t)stream) !=

@@ -374,6 +374,9 @@ class DeviceNetwork:
 
     def _finish(self) -> None:
         self.layer_devs = (_native.LayerDev * max(1, self.num_layers))()
+        # every layer launches a grid (no empty layout): the cross-layer path applies
+        self.launches_every_layer = self.num_layers > 0 and all(
+            pl.num_blocks > 0 for pl in self._plans_meta)
         for l, pl in enumerate(self._plans_meta):
             d = self.layer_devs[l]
             for k in _KINDS:
@@ -403,10 +406,19 @@ class DeviceNetwork:
         self.huge = float(np.ldexp(1.0, min(127, 95 - emax))) if emax < 95 else 0.0
 
 
+# Cross-layer overlap (spdnn_scratch's optional buffers): a layer starts on the
+# input tiles the previous one has published instead of waiting for its whole
+# grid. Opt-in (SPDNN_XL=1): measured on C2 it trims the per-inference fixed
+# cost but costs ~3 % per item, a net loss so far.
+CROSS_LAYER = __import__("os").environ.get("SPDNN_XL", "0") == "1"
+
+
 class Workspace:
     """Per-inference device buffers for a feature-count capacity (reused)."""
 
-    def __init__(self, neurons: int, m_cap: int, num_layers: int, device, buffers: int = 2):
+    def __init__(self, neurons: int, m_cap: int, num_layers: int, device, buffers: int = 2,
+                 xl: bool = False):
+        buffers = max(buffers, 3) if xl else buffers
         torch = _torch()
         self.neurons = neurons
         self.m_cap = m_cap
@@ -425,10 +437,21 @@ class Workspace:
         self.guard = torch.zeros(1, dtype=i32, device=device)
         self.scratch = _native.Scratch(self.tile_done.data_ptr(), self.tile_alive.data_ptr(),
                                        self.work.data_ptr(), self.guard.data_ptr())
+        self.xl = xl
+        if xl:
+            self.tile_done2 = torch.zeros_like(self.tile_done)
+            self.tile_alive2 = torch.zeros_like(self.tile_alive)
+            self.ready = torch.zeros((num_layers + 1) * (self.ld // 64), dtype=i32, device=device)
+            self.sync = torch.zeros(2 * (num_layers + 1), dtype=i32, device=device)
+            for f, t in (("y2", self.y[2]), ("a2", self.a[2]), ("cat2", self.cat[2]),
+                         ("tile_done2", self.tile_done2), ("tile_alive2", self.tile_alive2),
+                         ("ready", self.ready), ("sync", self.sync)):
+                setattr(self.scratch, f, t.data_ptr())
         self.iota = torch.arange(self.ld, dtype=i32, device=device)
 
-    def fits(self, neurons: int, m: int, num_layers: int) -> bool:
-        return neurons == self.neurons and m <= self.m_cap and num_layers <= self.num_layers
+    def fits(self, neurons: int, m: int, num_layers: int, xl: bool = False) -> bool:
+        return (neurons == self.neurons and m <= self.m_cap and num_layers <= self.num_layers
+                and xl == self.xl)
 
 
 _cache_lock = threading.Lock()
@@ -459,11 +482,12 @@ def workspace(neurons: int, m: int, num_layers: int) -> Workspace:
     key = (dev, threading.get_ident())
     with _cache_lock:
         ws = _ws_cache.get(key)
-        if ws is None or not ws.fits(neurons, m, num_layers):
+        if ws is None or not ws.fits(neurons, m, num_layers, CROSS_LAYER):
             ws = None
             _ws_cache.pop(key, None)
             torch.cuda.empty_cache()
-            ws = Workspace(neurons, max(m, 1), num_layers, torch.device("cuda", dev))
+            ws = Workspace(neurons, max(m, 1), num_layers, torch.device("cuda", dev),
+                           xl=CROSS_LAYER)
             _ws_cache[key] = ws
         return ws
 
@@ -474,11 +498,11 @@ def workspace(neurons: int, m: int, num_layers: int) -> Workspace:
 class DeviceRun:
     """State of one on-device inference after the layer loop."""
 
-    def __init__(self, ws: Workspace, num_layers: int, m0: int):
+    def __init__(self, ws: Workspace, num_layers: int, m0: int, nbufs: int = 2):
         self.ws = ws
         self.num_layers = num_layers
         self.m0 = m0
-        self.out_index = num_layers % 2
+        self.out_index = num_layers % nbufs
         self.fma = False
         self.guard = 0  # filled by collect(): bit 0 FMA-form guard, bit 1 non-finite input
 
@@ -519,19 +543,33 @@ def run_opts(net: DeviceNetwork, fma: bool | None = None) -> _native.RunOpts:
     return _native.RunOpts(int(use), net.tiny, FEATURES_PER_LANE)
 
 
+def reset_run(net: DeviceNetwork, ws: Workspace, m0: int) -> bool:
+    """Zero the per-run counters (stream-ordered); True when the run takes the
+    cross-layer path (final state in buffer num_layers % 3)."""
+    ws.counts.zero_()
+    ws.counts[0] = m0
+    ws.work.zero_()
+    # the cross-layer path needs every layer to launch (the C side falls back
+    # to the two-buffer path otherwise, and so must the output index)
+    xl = ws.xl and net.launches_every_layer and FEATURES_PER_LANE == 4
+    if xl:
+        ws.ready.zero_()
+        ws.sync.zero_()
+        ws.sync[0] = 1 << 30  # completion counter "before" the first layer: its input is final
+    return xl
+
+
 def run_layers(net: DeviceNetwork, ws: Workspace, m0: int, fma: bool | None = None
                ) -> DeviceRun:
     """Enqueue every layer on the current stream; no host synchronisation."""
     torch = _torch()
-    ws.counts.zero_()
-    ws.counts[0] = m0
-    ws.work.zero_()
+    xl = reset_run(net, ws, m0)
     opts = run_opts(net, fma)
     _native.check(_native.lib().spdnn_infer_layers(
         net.num_layers, net.layer_devs, _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
         _dptr(ws.a[0]), _dptr(ws.a[1]), _dptr(ws.cat[0]), _dptr(ws.cat[1]), _dptr(ws.counts),
         ctypes.byref(ws.scratch), ctypes.byref(opts), _stream_ptr(torch)), "spdnn_infer_layers")
-    run = DeviceRun(ws, net.num_layers, m0)
+    run = DeviceRun(ws, net.num_layers, m0, 3 if xl else 2)
     run.fma = bool(opts.fma_form)
     return run
 
