@@ -787,42 +787,59 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     const int kRes = P * 32 - 1;
     int m_fin = -1;   // resolver: the layer's final input count, once seen
     int pre = -1;     // resolver: early read of the next item's ready counter
-    auto resolve = [&](int t, int pre_v) -> int {
+    uint32_t pre_c = 0;  // resolver: early read of the previous layer's completion counter
+    // input final: the previous layer's counter reached kBig (checked first,
+    // so that the steady state switches to local validity at once)
+    auto take_final = [&]() {
+      fence_acq_rel();
+      m_fin = *reinterpret_cast<const volatile int32_t *>(A.m_in);
+      // the tile total joins this layer's completion counter exactly once
+      if (atomicCAS(A.added, 0u, 1u) == 0u) {
+        const uint32_t tl = (uint32_t)((m_fin + T - 1) / T);
+        red_add_u(A.cnt_out, kBig - tl);
+      }
+    };
+    auto resolve = [&](int t, int pre_v, uint32_t pre_cv) -> int {
+      if (m_fin < 0 && pre_cv == kBig) take_final();
       if (m_fin < 0 && pre_v >= T) {
         fence_acq_rel();
         return T;
       }
       for (uint32_t spin = 0;; spin++) {
         if (m_fin >= 0) return t * T < m_fin ? min(T, m_fin - t * T) : -1;
+        if (ld_relaxed_u(A.cnt_in) == kBig) {
+          take_final();
+          continue;
+        }
         if (A.ready_in && (int64_t)(t + 1) * T <= A.ld && ld_relaxed(A.ready_in + t) >= T) {
           fence_acq_rel();
           return T;
-        }
-        if (ld_relaxed_u(A.cnt_in) == kBig) {
-          fence_acq_rel();
-          m_fin = *reinterpret_cast<const volatile int32_t *>(A.m_in);
-          // the tile total joins this layer's completion counter exactly once
-          if (atomicCAS(A.added, 0u, 1u) == 0u) {
-            const uint32_t tl = (uint32_t)((m_fin + T - 1) / T);
-            red_add_u(A.cnt_out, kBig - tl);
-          }
-          continue;
         }
         __nanosleep(256);
         if (spin > (1u << 26)) __trap();  // the previous layer never published
       }
     };
-    auto preload = [&](int j) {  // resolver: early relaxed read for entry j
+    auto preload = [&](int j) {  // resolver: early relaxed reads for entry j
+      if (m_fin >= 0) return;
       const int t = item_of(j) / nb;
-      pre = (m_fin < 0 && A.ready_in && (int64_t)(t + 1) * T <= A.ld) ? ld_relaxed(A.ready_in + t)
-                                                                      : -1;
+      pre_c = ld_relaxed_u(A.cnt_in);
+      pre = (A.ready_in && (int64_t)(t + 1) * T <= A.ld) ? ld_relaxed(A.ready_in + t) : -1;
     };
     // once the input is final (the previous layer completed) every thread
     // derives validity from the count itself: no polls, fences or barrier
     int mf = -1;
     if (XL) {
       if (ptid == kRes) {
-        for (int j = 0; j < kMetaAhead; j++) s_valid[j] = resolve(item_of(j) / nb, -1);
+        // every counter read issued before the first use: one round trip
+        const uint32_t c0 = ld_relaxed_u(A.cnt_in);
+        int r0[kMetaAhead];
+#pragma unroll
+        for (int j = 0; j < kMetaAhead; j++) {
+          const int t = item_of(j) / nb;
+          r0[j] = (A.ready_in && (int64_t)(t + 1) * T <= A.ld) ? ld_relaxed(A.ready_in + t) : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < kMetaAhead; j++) s_valid[j] = resolve(item_of(j) / nb, r0[j], c0);
         preload(kMetaAhead);
         if (m_fin >= 0) s_mfin = m_fin;
       }
@@ -1016,7 +1033,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       if (XL) {
         if (mf < 0) {  // uniform: every producer thread updates mf after the same barrier
           if (ptid == kRes) {
-            s_valid[(k + kMetaAhead) & 7] = resolve(item_of(k + kMetaAhead) / nb, pre);
+            s_valid[(k + kMetaAhead) & 7] = resolve(item_of(k + kMetaAhead) / nb, pre, pre_c);
             preload(k + kMetaAhead + 1);  // claimed at the top of this iteration
             if (m_fin >= 0) s_mfin = m_fin;
           }
