@@ -867,6 +867,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
       pbar();
       mf = s_mfin;
+      if (mf >= 0) {  // input final: the classic bounds from here on
+        M = mf;
+        items = (int)((M + T - 1) / T) * nb;
+      }
       fence_proxy_async();
       for (int j = 0; j < kMetaAhead; j++) {
         if (s_valid[j] <= 0) continue;
@@ -911,7 +915,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       cp_async_wait<1>();
       pbar();
       const int item = item_of(k);
-      if (XL ? s_valid[k & 7] < 0 : item >= items) {
+      if ((XL && mf < 0) ? s_valid[k & 7] < 0 : item >= items) {
         cp_async_wait<0>();
         if (pw == 0) {
           // end markers in the next nbuf entries; a consumer warp waits at most
@@ -937,7 +941,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const int *ain = en + 8;
       const int *sfp = en + 8 + T;
       // feature columns 32q + lane (q < FPL) of tile t
-      const int valid = XL ? s_valid[k & 7] : min(T, M - t * T);
+      const int valid = (XL && mf < 0) ? s_valid[k & 7] : min(T, M - t * T);
       int src[FPL];
 #pragma unroll
       for (int q = 0; q < FPL; q++) src[q] = 32 * q + lane < valid ? ain[32 * q + lane] : -1;
@@ -1062,6 +1066,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
           }
           pbar();
           mf = s_mfin;
+          if (mf >= 0) {
+            M = mf;
+            items = (int)((M + T - 1) / T) * nb;
+          }
           fence_proxy_async();
           v_ahead = s_valid[(k + kMetaAhead) & 7];
         } else {
