@@ -1097,8 +1097,9 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     // a_out / cat_out (pruning without a pass over Y).
     // Cross-layer mode: a finished tile's survivors are announced to the next
     // layer (per next-layer tile) and the tile counted complete once the
-    // stores are fenced -- done one entry later, after that entry's slot has
-    // gone back to the producer, so the fence never delays a slot release.
+    // stores are fenced -- at the top of the next iteration, where the
+    // publisher would otherwise wait for the next entry, so the fence does
+    // not sit between an entry's completion and its slot release.
     // The counter reaching kBig is the next layer's "input final".
     int pend_base = 0, pend_tot = -1;
     auto publish = [&]() {
@@ -1116,6 +1117,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       pend_tot = -1;
     };
     for (int k = 0;; k++) {
+      publish();  // the tile the previous entry completed, before waiting for this one
       const int slot = k % nbuf;
       const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
       mbar_wait(full0 + 8 * slot, phase);
@@ -1147,7 +1149,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         if (lane == q) wv = word;
       }
       if (lane == 0) mbar_arrive(free0 + 8 * slot);
-      publish();  // the previous entry's tile, if it completed one
       if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * t + lane], wv);
       __syncwarp();
       int last = 0;
