@@ -914,6 +914,16 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
       cp_async_wait<1>();
       pbar();
+      bool was_early = false;  // cross-layer: the input was not final before this barrier
+      if (XL && mf < 0) {
+        was_early = true;
+        mf = s_mfin;  // the resolver writes it before arriving here
+        if (mf >= 0) {  // input final: the classic bounds from here on
+          M = mf;
+          items = (int)((M + T - 1) / T) * nb;
+        }
+        fence_proxy_async();  // the resolver's acquires reach this thread's TMA reads
+      }
       const int item = item_of(k);
       if ((XL && mf < 0) ? s_valid[k & 7] < 0 : item >= items) {
         cp_async_wait<0>();
@@ -1057,28 +1067,27 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       // ring entry k's slot is reused by k + kMetaRing > k + kMetaAhead only.
       // Issued after the header went out: off the slot turnaround path.
       int v_ahead = 1;
+      bool ain_now = true;
       if (XL) {
-        if (mf < 0) {  // uniform: every producer thread updates mf after the same barrier
+        // item k+kMetaAhead-1 was resolved in the previous iteration, before
+        // this iteration's barrier: while the input is not final its feature
+        // columns are fetched one iteration late (no extra barrier)
+        if ((mf < 0 || was_early) && s_valid[(k + kMetaAhead - 1) & 7] > 0)
+          prefetch_desc(k + kMetaAhead - 1, false, true);
+        if (mf < 0) {
           if (ptid == kRes) {
             s_valid[(k + kMetaAhead) & 7] = resolve(tile_of(item_of(k + kMetaAhead)), pre, pre_c);
             preload(k + kMetaAhead + 1);  // claimed at the top of this iteration
             if (m_fin >= 0) s_mfin = m_fin;
           }
-          pbar();
-          mf = s_mfin;
-          if (mf >= 0) {
-            M = mf;
-            items = (int)((M + T - 1) / T) * nb;
-          }
-          fence_proxy_async();
-          v_ahead = s_valid[(k + kMetaAhead) & 7];
+          ain_now = false;
         } else {
           const int ta = tile_of(item_of(k + kMetaAhead));
           v_ahead = ta * T < mf ? min(T, mf - ta * T) : -1;
           if (ptid == kRes) s_valid[(k + kMetaAhead) & 7] = v_ahead;
         }
       }
-      prefetch_desc(k + kMetaAhead, true, v_ahead > 0);
+      prefetch_desc(k + kMetaAhead, true, ain_now && v_ahead > 0);
       prefetch_fp(k + kFpAhead);
       cp_async_commit();
       PROF_MARK(5);  // [5] header
