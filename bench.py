@@ -1,14 +1,15 @@
 #!/usr/bin/env python
 """Benchmark: TeraEdges/s of the sparse-DNN inference hot path on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
 
-Workload (BASELINE.json configs[1], the single-B200 configuration the metric
-is quoted on): Graph-Challenge-style synthetic network, 4096 neurons x 480
-layers, 32 connections per neuron, weights 1/16, bias -0.35; 60000 binary
-inputs with density 0.35 (= |bias|, SURVEY.md section 0 finding 4; the
-generator is the reference's, bit for bit). One step = one full inference
-(all 480 layers with pruning) over the 60000-input batch.
+Workload (BASELINE.json configs[2], the configuration the metric "TeraEdges/s
+at 1/2/4/8 B200" is quoted on; it fits one GPU): Graph-Challenge-style
+synthetic network, 16384 neurons x 1920 layers, 32 connections per neuron,
+weights 1/16, bias -0.4; 60000 binary inputs with density 0.4 (= |bias|,
+SURVEY.md section 0 finding 4; the generator is the reference's, bit for
+bit). One step = one full inference (all 1920 layers with pruning) over the
+60000-input batch. `--config c1|c2|c4|c5` selects the other configs.
 
 metric  : credited TeraEdges/s = 60000 * sum(nnz) / step time (the
           reference's and the paper's convention, spdnn/engine.py:290,
@@ -21,11 +22,17 @@ e2e     : the same metric through the public API (engine.infer on a
 roofline: the layer kernel (csrc/layer.cu), bytes per launch
           = 8*N*M_l + 6*nnz_l + 4*N, over the kernel's
           CUDA-event time measured around every launch in the timed steps.
-cpu_baseline / --impl reference: the oracle port (oracle/spdnn_oracle.c) on
-          the host cores, on a bounded column sample of the same workload.
+cpu_baseline: the oracle port (oracle/spdnn_oracle.c) on the host cores, on a
+          bounded column sample of the same workload.
+--impl reference: the unmodified reference (baseline/_ref: spdnn.parallel.
+          run_batch_parallel with one worker per host core) on a bounded
+          sample, next to the port (run_reference).
 
-N > 1 (torchrun): batch-parallel over ranks (paper section "Multi-GPU";
-spdnn/parallel.py): the 60000 inputs are partitioned, weights replicated.
+--gpus N > 1: relaunched under torch.distributed.run with N local ranks
+(or launched that way by the driver): batch-parallel over ranks (paper
+section "Multi-GPU"; spdnn/parallel.py): the 60000 inputs are partitioned,
+weights replicated, counts allgathered over NCCL, categories gathered to
+rank 0; time = max over ranks.
 """
 
 from __future__ import annotations
@@ -71,6 +78,14 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def init_nccl_log():
+    """NCCL's communicator-init lines (`nRanks N`) on stderr, so the run shows
+    how many ranks the communicator really had; stdout keeps the JSON line."""
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 
 def build_workload(cfg, rank=0, world=1):
@@ -213,7 +228,7 @@ def run_reference_streamed(args, cfg):
     return v, orc.seconds, len(cols), threads, (
         f"{len(cols)} fixed-seed columns of {cfg['inputs']} through all {cfg['layers']} "
         f"layers, generated and run layer by layer (oracle/spdnn_oracle.c, {threads} threads, "
-        f"{orc.seconds:.1f} s of oracle time)")
+        f"{orc.seconds:.1f} s of oracle time)"), orc.counts
 
 
 def _sample_columns(cfg, cols):
@@ -227,52 +242,127 @@ def _sample_columns(cfg, cols):
     return out
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_spdnn(cfg, port_counts, port_cols: int, workers: int, target_s: float = 10.0):
+    """The unmodified reference (baseline/_ref, `spdnn` + numba) through its own
+    public API, spdnn.parallel.run_batch_parallel(..., InferenceConfig(workers=
+    host cores)), on a bounded sample: the first `cols` inputs through the
+    network's first `lp` layers (its per-layer ELL preparation, ~0.26 s/layer
+    at 16384 neurons, keeps the whole network out of reach of one bench run).
+    Its active-edge rate (sum over layers of active_before * nnz / the
+    reference's own elapsed_seconds) is extrapolated to the full network with
+    the port's per-layer count sequence of the same inputs:
+      t_full = sum_l count_l * nnz_l / rate,  TE/s = port_cols * sum nnz / t_full.
+    Returns None when the reference is not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "spdnn")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        from spdnn import ingest as ring, parallel as rpar
+        from spdnn.engine import prepare_model as rprep
+        from spdnn.model import InferenceConfig as RConf, make_feature_batch as rbatch
+    except ImportError as e:  # numba missing on this host
+        log(f"reference not importable: {e}")
+        return None
+    n = cfg["neurons"]
+    nnz_layer = n * K_CONN
+    cols = int(min(cfg["inputs"], max(48 * workers, 512)))
+    # layers: ELL preparation time ~ n * 16 us per layer; keep it near 10 s
+    lp = int(max(4, min(cfg["layers"], 10.0 / (n * 16e-6))))
+    t0 = time.perf_counter()
+    model = ring.generate_synthetic_network(ring.GeneratorSpec(
+        neurons=n, layers=lp, connections_per_neuron=K_CONN, bias_value=cfg["bias"],
+        seed=MODEL_SEED))
+    conf = RConf(workers=workers)
+    prepared = rprep(model, conf, "optimized")
+    t_prep = time.perf_counter() - t0
+    data = _sample_columns(cfg, np.arange(cols))
+    batch = rbatch(n, data)
+    # numba JIT / cache load outside the clock
+    rpar.run_batch_parallel(model, rbatch(n, data[:, :min(cols, 2 * workers)]), conf,
+                            prepared=prepared)
+    rates, secs = [], 0.0
+    while secs < target_s or not rates:
+        res, _, _ = rpar.run_batch_parallel(model, batch, conf, prepared=prepared)
+        active_edges = sum(o.active_before for o in res.per_layer) * nnz_layer
+        rates.append(active_edges / res.elapsed_seconds)
+        secs += res.elapsed_seconds
+    rate = float(np.median(rates))
+    L = cfg["layers"]
+    t_full = float(np.sum(np.asarray(port_counts[:L], np.float64))) * nnz_layer / rate
+    value = port_cols * L * nnz_layer / t_full / 1e12
+    return {"value": value, "unit": "TE/s", "cores": workers, "kind": "reference",
+            "active_edge_rate_G": rate / 1e9,
+            "sample": f"spdnn.parallel.run_batch_parallel (baseline/_ref, numba) with "
+                      f"{workers} workers on the first {cols} inputs x first {lp} of {L} "
+                      f"layers ({len(rates)} runs, {secs:.1f} s; ELL prep {t_prep:.1f} s "
+                      f"untimed); active-edge rate {rate / 1e9:.2f} G/s extrapolated over "
+                      f"the port's per-layer counts of the first {port_cols} inputs",
+            "cpu_model": cpu_model()}
+
+
 def run_reference(args, cfg):
+    """--impl reference: rank 0 times the reference's CPU path on the host
+    cores. The line's value is the unmodified reference (reference_spdnn,
+    kind "reference") when baseline/_ref imports, else the C port
+    (oracle/spdnn_oracle.c, kind "port"); the port's own figure is always
+    reported under "port" (it also supplies the per-layer counts the
+    reference's rate is extrapolated over)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    if cfg.get("chunked"):
-        v, secs, sample, threads, what = run_reference_streamed(args, cfg)
-        print(json.dumps({
-            "metric": "TeraEdges/s", "impl": "reference", "value": v, "unit": "TE/s",
-            "n_gpus": world, "steps": 1, "warmup": 0, "ms_per_step": secs * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
-                       "input_density": cfg["density"], "sample_inputs": sample},
-            "cpu_baseline": {"value": v, "unit": "TE/s", "cores": threads, "kind": "port",
-                             "sample": what},
-            "e2e": {"value": v, "unit": "TE/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}), flush=True)
-        return
-    if cfg.get("stress"):
-        model, _ = build_workload(dict(cfg, inputs=0))
-        inputs = stress_inputs(cfg)
-    else:
-        model, inputs = build_workload(cfg)
     threads = os.cpu_count() or 1
-    sample = args.cpu_sample
-    vals, secs = [], []
-    for _ in range(args.steps):
-        r = cpu_baseline(model, inputs, sample, threads, target_s=args.cpu_seconds)
-        sample = r["sample_cols"]
-        vals.append(r["value"])
-        secs.append(r["seconds"])
-    v = float(np.median(vals))
-    edges_full = cfg["inputs"] * sum(l.nnz for l in model.layers)
+    if cfg.get("chunked"):
+        v, secs, sample, _, what, counts = run_reference_streamed(args, cfg)
+        steps, warmup = 1, 0
+    else:
+        if cfg.get("stress"):
+            model, _ = build_workload(dict(cfg, inputs=0))
+            inputs = stress_inputs(cfg)
+        else:
+            model, inputs = build_workload(cfg)
+        sample = args.cpu_sample
+        vals, secs_l = [], []
+        for _ in range(args.steps):
+            r = cpu_baseline(model, inputs, sample, threads, target_s=args.cpu_seconds)
+            sample = r["sample_cols"]
+            vals.append(r["value"])
+            secs_l.append(r["seconds"])
+        v, secs, counts = float(np.median(vals)), float(np.median(secs_l)), r["counts"]
+        steps, warmup = args.steps, args.warmup
+        edges_full = cfg["inputs"] * sum(l.nnz for l in model.layers)
+        what = (f"first {sample} of {cfg['inputs']} inputs through all {cfg['layers']} layers "
+                f"(oracle/spdnn_oracle.c, {threads} threads); full-batch time extrapolates to "
+                f"{edges_full / (v * 1e12):.1f} s")
+        del model, inputs
+    port = {"value": v, "unit": "TE/s", "cores": threads, "kind": "port", "sample": what,
+            "cpu_model": cpu_model()}
+    ref = None if args.port_only else reference_spdnn(cfg, counts, sample, threads)
+    base = ref if ref is not None else port
     line = {
-        "metric": "TeraEdges/s", "impl": "reference", "value": v, "unit": "TE/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(np.median(secs)) * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "metric": "TeraEdges/s", "impl": "reference", "value": base["value"], "unit": "TE/s",
+        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": secs * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["name"], "inputs": cfg["inputs"],
                    "input_density": cfg["density"], "sample_inputs": sample},
-        "cpu_baseline": {"value": v, "unit": "TE/s", "cores": threads, "kind": "port",
-                         "sample": f"first {sample} of {cfg['inputs']} inputs through all "
-                                   f"{cfg['layers']} layers (oracle/spdnn_oracle.c, "
-                                   f"{threads} threads); full-batch time extrapolates to "
-                                   f"{edges_full / (v * 1e12):.1f} s"},
-        "e2e": {"value": v, "unit": "TE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": base, "port": port,
+        "e2e": {"value": base["value"], "unit": "TE/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -293,6 +383,7 @@ def run_ours_multi(args, cfg):
     # one rank per GPU over NCCL; SPDNN_DIST_BACKEND=gloo lets several ranks
     # share one GPU (test boxes with a single device)
     backend = os.environ.get("SPDNN_DIST_BACKEND", "nccl")
+    init_nccl_log()
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist.init_process_group(backend, init_method="env://")
@@ -372,6 +463,8 @@ def run_ours_multi(args, cfg):
             "config": {"workload": cfg["name"], "inputs": total,
                        "input_density": cfg["density"], "survivors": int(len(res.categories)),
                        "sum_active": int(sum_active), "parallelism": f"batch-parallel x{world}",
+                       "process_group": {"backend": dist.get_backend(),
+                                         "world_size": dist.get_world_size()},
                        "l2": "inputs larger than L2",
                        "imbalance_max_before": max(ratios) if ratios else 1.0,
                        "rebalances": sum(e.rebalanced for e in bal.entries),
@@ -748,6 +841,7 @@ def run_stress(args, cfg):
 
     rank, world, local = dist_env()
     if world > 1:
+        init_nccl_log()
         torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
         dist.init_process_group(os.environ.get("SPDNN_DIST_BACKEND", "nccl"),
                                 init_method="env://")
@@ -814,12 +908,28 @@ def run_stress(args, cfg):
         dist.destroy_process_group()
 
 
+def relaunch_command(argv, gpus: int, port: int | None = None):
+    """`--gpus N` without a torchrun environment: the same command under
+    torch.distributed.run with N local ranks (one per GPU), rendezvous on
+    127.0.0.1. Returns None when no relaunch is needed."""
+    if gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if port is None:
+        import socket
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__)] + list(argv)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dump-layers", default="", help="write per-layer counts/times (JSON)")
     ap.add_argument("--plan", default="", help="layout knobs, e.g. max_groups=8,footprint_cap=96")
@@ -827,9 +937,19 @@ def main():
                     help="inputs in the CPU-baseline sample (0 = skip the CPU leg)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="grow the CPU sample to about this much CPU time (0 = fixed sample)")
+    ap.add_argument("--port-only", action="store_true",
+                    help="reference arm: time only the C port, not baseline/_ref's spdnn")
     ap.add_argument("--inputs", type=int, default=0,
                     help="override the batch size (diagnostics: e.g. one rank's share at N=8)")
     args = ap.parse_args()
+    cmd = relaunch_command(sys.argv[1:], args.gpus)
+    if cmd is not None:
+        # one process per GPU; rank 0 prints the single JSON line
+        log("relaunching: " + " ".join(cmd))
+        sys.exit(subprocess.call(cmd))
+    rank, world, _ = dist_env()
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE")
     if args.warmup < 3 and args.impl == "ours":
         log("warning: fewer than 3 warm-up steps")
     cfg = CONFIGS[args.config]

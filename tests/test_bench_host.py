@@ -52,3 +52,43 @@ def test_balance_summary_load_model():
     rep2 = parallel.BalanceReport(entries=[mk(0, [8, 2], [8, 2], 0), mk(1, [6, 2], [6, 2], 0)])
     s2 = bench.balance_summary(rep2, [10, 10])
     assert abs(s2["time_weighted_max_over_mean"] - (10 + 8) / (10 + 5)) < 1e-12
+
+
+def test_relaunch_command():
+    """--gpus N without a torchrun environment re-executes the same command
+    under torch.distributed.run with N local ranks on 127.0.0.1."""
+    env = dict(os.environ)
+    try:
+        os.environ.pop("WORLD_SIZE", None)
+        assert bench.relaunch_command(["--gpus", "1"], 1) is None
+        cmd = bench.relaunch_command(["--gpus", "4", "--config", "c3"], 4, port=29555)
+        assert cmd[1:3] == ["-m", "torch.distributed.run"]
+        assert "--nproc-per-node=4" in cmd and "--master-addr=127.0.0.1" in cmd
+        assert "--master-port=29555" in cmd
+        assert cmd[-4:] == [os.path.abspath(bench.__file__), "--gpus", "4", "--config", "c3"][-4:]
+        os.environ["WORLD_SIZE"] = "4"  # already under torchrun: no relaunch
+        assert bench.relaunch_command(["--gpus", "4"], 4) is None
+    finally:
+        os.environ.clear()
+        os.environ.update(env)
+
+
+def test_gpus2_launch_on_cpu():
+    """`bench.py --gpus 2` really starts two ranks (torchrun, world size 2):
+    the reference arm runs on rank 0 only, which prints one JSON line with
+    n_gpus 2; rank 1 exits 0 without work."""
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run(
+        [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+         "--config", "c1", "--steps", "1", "--warmup", "0", "--port-only",
+         "--cpu-sample", "16", "--cpu-seconds", "0"],
+        capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference" and d["value"] > 0
+    assert "relaunching" in out.stderr

@@ -270,27 +270,6 @@ def test_nonfinite_inputs_rerun_unpadded(cuda_ok):
     assert np.array_equal(a[ok].view(np.uint32), b[ok].view(np.uint32))
 
 
-@pytest.mark.slow
-def test_config3_full_network_sampled_columns(cuda_ok):
-    """BASELINE.json configs[2] network at full size (16384 neurons x 1920
-    layers, bias -0.4, density 0.4): the GPU run of 4096 inputs agrees with the
-    oracle on a fixed-seed sample of 96 of them (columns are independent, so
-    the sample's categories and values must match exactly)."""
-    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
-        neurons=16384, layers=1920, connections_per_neuron=32, bias_value=-0.4, seed=1))
-    inputs = ingest.generate_synthetic_inputs(16384, 4096, 0.4, seed=2)
-    res = engine.infer(model, inputs, InferenceConfig())
-    pick = np.sort(np.random.default_rng(123).choice(4096, 96, replace=False))
-    sub = make_feature_batch(16384, np.asfortranarray(inputs.data[:, pick]),
-                             categories=pick, total_inputs=4096)
-    ref = oracle.infer(model, sub, threads=os.cpu_count() or 1)
-    got = np.intersect1d(res.categories, pick)
-    assert got.tolist() == ref.categories.tolist()
-    assert 0 < len(got) < len(pick)  # partial survival at density = |bias|
-    pos = np.searchsorted(res.categories, ref.categories)
-    assert same_bits(np.asarray(res.final.data)[:, pos], ref.final)
-
-
 def _streaming_case(layers=40, m=1500, bias=-0.3, seed=4):
     model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
         neurons=1024, layers=layers, connections_per_neuron=32, bias_value=bias, seed=seed))
@@ -410,27 +389,6 @@ def test_two_features_per_lane_variant(cuda_ok, monkeypatch):
     assert same_bits(got.final.data, want.final.data)
     ref = oracle.infer(model, inputs, threads=4)
     assert got.categories.tolist() == ref.categories.tolist()
-
-
-def test_config2_full_size_sampled_columns(cuda_ok):
-    """BASELINE.json configs[1] at full size (4096 x 480, bias -0.35, 60000
-    inputs at density 0.35): the full GPU run's survivors within a fixed-seed
-    sample of 160 inputs equal the oracle's, and the GPU run of the sample
-    alone is bit-identical (values and per-layer counts)."""
-    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
-        neurons=4096, layers=480, connections_per_neuron=32, bias_value=-0.35, seed=1))
-    inputs = ingest.generate_synthetic_inputs(4096, 60000, 0.35, seed=2)
-    full = engine.infer(model, inputs, InferenceConfig(), values=False)
-    assert len(full.categories) == 30924  # bench's survivors (profiles/r1_bench_c2.json)
-    pick = np.sort(np.random.default_rng(321).choice(60000, 160, replace=False))
-    sub = make_feature_batch(4096, np.asfortranarray(inputs.data[:, pick]), categories=pick,
-                             total_inputs=60000)
-    ref = oracle.infer(model, sub, threads=os.cpu_count() or 1)
-    assert np.intersect1d(full.categories, pick).tolist() == ref.categories.tolist()
-    got = engine.infer(model, sub, InferenceConfig())
-    assert got.categories.tolist() == ref.categories.tolist()
-    assert same_bits(got.final.data, ref.final)
-    assert [o.active_before for o in got.per_layer] + [len(got.categories)] == ref.counts.tolist()
 
 
 def _window_layer(rng, n, k, weights):
