@@ -674,7 +674,7 @@ def run_ours(args, cfg):
         engine.stage_inputs(ws, x_dev, cats_dev, net)
         if evs is None:
             return engine.run_layers(net, ws, m)
-        xl = engine.reset_run(net, ws, m)
+        engine.reset_run(ws, m)
         # the whole layer loop in one C call (spdnn_infer_layers_timed), an
         # event recorded before every layer: launches are not paced by Python
         handles = evs
@@ -684,7 +684,7 @@ def run_ours(args, cfg):
             engine._dptr(ws.cat[0]), engine._dptr(ws.cat[1]), engine._dptr(ws.counts),
             ctypes.byref(ws.scratch), ctypes.byref(opts), sp, handles),
             "spdnn_infer_layers_timed")
-        return engine.DeviceRun(ws, L, m, 3 if xl else 2)
+        return engine.DeviceRun(ws, L, m)
 
     # correctness of the timed configuration: categories after one step
     run0 = step()

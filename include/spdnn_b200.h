@@ -57,7 +57,7 @@ enum {
 /* ---- one-time layout conversion (host, C++) ----------------------------- */
 
 typedef struct spdnn_plan_params {
-  int32_t rows_per_group;   /* R in {1, 3, 6, 7}; 0 = choose per layer */
+  int32_t rows_per_group;   /* R in {1, 3, 4, 5, 6, 7}; 0 = choose per layer */
   int32_t footprint_cap;    /* max input neurons staged per block stage */
   int32_t max_groups;       /* max row groups per block (<= warps per CTA) */
   int32_t record_cap;       /* max union records staged per block stage */
@@ -159,20 +159,6 @@ typedef struct spdnn_scratch {
   uint32_t *guard;         /* [1] zero-initialised; bit 0 = FMA-form guard
                               tripped (rerun in the exact form), bit 1 =
                               non-finite input (rerun with one row per group) */
-  /* Optional, all set or all null: cross-layer overlap in spdnn_infer_layers.
-   * Layer l+1's CTAs (started by programmatic dependent launch as SMs free up)
-   * take an input tile as soon as layer l has published its survivors instead
-   * of waiting for layer l's whole grid. Buffers rotate over three (y2, a2,
-   * cat2: layer l+1 writes columns layer l may still read), the final state
-   * is in buffer num_layers % 3. */
-  float *y2;               /* like y0/y1 */
-  int32_t *a2;
-  int64_t *cat2;
-  int32_t *tile_done2;     /* second tile set (consecutive layers alternate) */
-  uint32_t *tile_alive2;
-  int32_t *ready;          /* [(num_layers + 1) * (ld / 64)] zero-initialised */
-  uint32_t *sync;          /* [2 * (num_layers + 1)] zero-initialised, then sync[0] =
-                              2^30 (per-layer completion counters, then CAS flags) */
 } spdnn_scratch;
 
 /* Arithmetic form of a launch (layer.cu):
@@ -207,8 +193,7 @@ int spdnn_layer_forward(const spdnn_layer_dev *layer, const float *bias,
 /* All layers back to back on `stream` (engine.infer's loop, engine.py:264-285).
  * Buffers ping-pong between index 0 and 1; counts[l] = active features
  * entering layer l (counts[0] must hold M_0; counts[1..L] zeroed by caller).
- * The final state is in buffer (num_layers % 2) -- (num_layers % 3) when the
- * scratch carries the cross-layer buffers (and every layer has blocks). */
+ * The final state is in buffer (num_layers % 2). */
 int spdnn_infer_layers(int64_t num_layers, const spdnn_layer_dev *layers,
                        const float *bias, float *y0, float *y1, int64_t ld,
                        int32_t *a0, int32_t *a1, int64_t *cat0, int64_t *cat1,

@@ -54,10 +54,7 @@ class LayerDev(ctypes.Structure):
 
 
 class Scratch(ctypes.Structure):
-    _fields_ = [("tile_done", P), ("tile_alive", P), ("work", P), ("guard", P),
-                # optional cross-layer overlap buffers (include/spdnn_b200.h)
-                ("y2", P), ("a2", P), ("cat2", P), ("tile_done2", P), ("tile_alive2", P),
-                ("ready", P), ("sync", P)]
+    _fields_ = [("tile_done", P), ("tile_alive", P), ("work", P), ("guard", P)]
 
 
 class RunOpts(ctypes.Structure):

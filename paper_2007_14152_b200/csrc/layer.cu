@@ -177,44 +177,6 @@ struct FastDiv {
   }
 };
 
-// ---- cross-layer readiness (LayerArgs::xl) ----------------------------------
-constexpr uint32_t kBig = 1u << 30;  // completion counter target (see publisher)
-__device__ __forceinline__ int ld_relaxed(const int32_t *p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t ld_relaxed_u(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_acq_rel() {
-#ifndef SPDNN_XL_NO_ACQ_FENCE
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#endif
-}
-__device__ __forceinline__ void fence_proxy_async() {
-#ifndef SPDNN_XL_NO_PROXY_FENCE
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-#endif
-}
-__device__ __forceinline__ void st_release_u(uint32_t *p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t atom_add_acq_rel_u(uint32_t *p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v)
-               : "memory");
-  return old;
-}
-__device__ __forceinline__ void red_add_u(uint32_t *p, uint32_t v) {
-  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void red_add_release(int32_t *p, int32_t v) {
-  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 // TMA tile gather: rows r0..r3 of the 2-D tensor, columns [col, col + box),
 // into 4 consecutive smem rows; completion as tx bytes on `bar`
 __device__ __forceinline__ void tma_gather4(uint32_t sdst, const CUtensorMap *tmap, int col,
@@ -293,17 +255,6 @@ struct LayerArgs {
   int simple_wait;     // 1: consumer warps visit every (C/gpi)-th entry and (C/gpi) | nbuf
   int gpi;             // consumer work units (row groups) per item = max groups per block
   uint32_t act_off;    // activity bytes: [nbuf][gpi][32 lanes], one byte per lane and unit
-  // Cross-layer mode (xl = 1, spdnn_infer_layers with the scratch's xl buffers):
-  // no griddepcontrol.wait -- an item's input tile is used as soon as it is
-  // published. ready_in[t] counts the survivors the previous layer appended
-  // to positions [T t, T t + T); *cnt_in == kBig once m_in is final and every
-  // append is done. This layer publishes the same for the next one.
-  int xl;
-  const int32_t *ready_in;  // null for the first layer (its input is final)
-  int32_t *ready_out;
-  const uint32_t *cnt_in;  // the previous layer's cnt_out (kBig from the start: first layer)
-  uint32_t *cnt_out;  // completed tiles + (kBig - tiles) once the tile total is known
-  uint32_t *added;    // CAS flag: the tile total was added to cnt_out
 };
 
 // Ring-buffer header written by the producer (one per buffer fill).
@@ -311,7 +262,7 @@ struct Header {
   int item;     // -1: no more work
   int entry;    // ring entry number (stale-phase check)
   int t, b;
-  int nst;      // cross-layer mode: | features of the tile that exist (1..T) << 16
+  int nst;
   int ng;
   int rec_cnt;  // records of this stage (multi-stage: all belong to group 0)
   int fp_cnt;
@@ -337,6 +288,34 @@ struct Rec<3> {
     w[0] = __uint_as_float(a.y);
     w[1] = __uint_as_float(a.z);
     w[2] = __uint_as_float(a.w);
+  }
+};
+// R = 4 and 5 share the 8-word record of R = 6 (offset + up to 7 weights)
+template <>
+struct Rec<4> {
+  static constexpr int W = 8;
+  __device__ __forceinline__ static void load(const uint32_t *p, uint32_t &off, float *w) {
+    uint4 a = *reinterpret_cast<const uint4 *>(p);
+    uint4 b = *reinterpret_cast<const uint4 *>(p + 4);
+    off = a.x;
+    w[0] = __uint_as_float(a.y);
+    w[1] = __uint_as_float(a.z);
+    w[2] = __uint_as_float(a.w);
+    w[3] = __uint_as_float(b.x);
+  }
+};
+template <>
+struct Rec<5> {
+  static constexpr int W = 8;
+  __device__ __forceinline__ static void load(const uint32_t *p, uint32_t &off, float *w) {
+    uint4 a = *reinterpret_cast<const uint4 *>(p);
+    uint4 b = *reinterpret_cast<const uint4 *>(p + 4);
+    off = a.x;
+    w[0] = __uint_as_float(a.y);
+    w[1] = __uint_as_float(a.z);
+    w[2] = __uint_as_float(a.w);
+    w[3] = __uint_as_float(b.x);
+    w[4] = __uint_as_float(b.y);
   }
 };
 template <>
@@ -665,9 +644,7 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
   }
 }
 
-// XL: cross-layer mode (LayerArgs::xl), a separate instantiation so that the
-// classic kernel carries none of its code
-template <int R, bool FMA, int FPL, bool MASK, bool XL>
+template <int R, bool FMA, int FPL, bool MASK>
 __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
@@ -678,8 +655,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   __shared__ unsigned long long s_tfirst[kMaxBufs];
 #endif
   __shared__ int s_items[8];  // producer: item index of ring entry j (j & 7)
-  __shared__ int s_valid[8];  // producer, cross-layer mode: features of entry j's tile, -1 = none
-  __shared__ int s_mfin;      // producer, cross-layer mode: final input count once seen, else -1
 
   using G = Geo<FPL, MASK>;
   constexpr int RW = MASK ? 1 : Rec<R>::W, T = G::kTileF, C = G::kC, P = G::kP, H = FPL / 2;
@@ -706,7 +681,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
 
   if (tid == 0) {
     s_wmask = __uint_as_float(A.L.weight_bits);
-    s_mfin = -1;
     for (int i = 0; i < nbuf; i++) {
       mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
       mbar_init(empty0 + 8 * i, gpi);  // one arrival per work unit (row group) of the item
@@ -715,7 +689,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (!XL && (warp < C || warp >= C + P)) {
+  if (warp < C || warp >= C + P) {
     dep_wait();
     if (M <= 0) return;
   }
@@ -799,88 +773,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     pbar();
     for (int j = 0; j < kFpAhead; j++) prefetch_fp(j);
     cp_async_commit();
-    // Cross-layer mode: one producer thread (the resolver, which has no copy
-    // duties) decides for each claimed item whether its input tile exists
-    // and has been published, polling the previous layer's counters. Its
-    // relaxed read of the next item's counter is issued one iteration early
-    // so that the steady state pays no round trip; a fence turns the read
-    // into an acquire, the producers' named barrier carries it to the other
-    // threads and fence.proxy.async to their TMA reads of the rows.
-    const int kRes = P * 32 - 1;
-    int m_fin = -1;   // resolver: the layer's final input count, once seen
-    int pre = -1;     // resolver: early read of the next item's ready counter
-    uint32_t pre_c = 0;  // resolver: early read of the previous layer's completion counter
-    // input final: the previous layer's counter reached kBig (checked first,
-    // so that the steady state switches to local validity at once)
-    auto take_final = [&]() {
-      fence_acq_rel();
-      m_fin = *reinterpret_cast<const volatile int32_t *>(A.m_in);
-      // the tile total joins this layer's completion counter exactly once
-      if (atomicCAS(A.added, 0u, 1u) == 0u) {
-        const uint32_t tl = (uint32_t)((m_fin + T - 1) / T);
-        red_add_u(A.cnt_out, kBig - tl);
-      }
-    };
-    auto resolve = [&](int t, int pre_v, uint32_t pre_cv) -> int {
-      if (m_fin < 0 && pre_cv == kBig) take_final();
-      if (m_fin < 0 && pre_v >= T) {
-        fence_acq_rel();
-        return T;
-      }
-      for (uint32_t spin = 0;; spin++) {
-        if (m_fin >= 0) return t * T < m_fin ? min(T, m_fin - t * T) : -1;
-        if (ld_relaxed_u(A.cnt_in) == kBig) {
-          take_final();
-          continue;
-        }
-        if (A.ready_in && (int64_t)(t + 1) * T <= A.ld && ld_relaxed(A.ready_in + t) >= T) {
-          fence_acq_rel();
-          return T;
-        }
-        __nanosleep(256);
-        if (spin > (1u << 26)) __trap();  // the previous layer never published
-      }
-    };
-    auto preload = [&](int j) {  // resolver: early relaxed reads for entry j
-      if (m_fin >= 0) return;
-      const int t = tile_of(item_of(j));
-      pre_c = ld_relaxed_u(A.cnt_in);
-      pre = (A.ready_in && (int64_t)(t + 1) * T <= A.ld) ? ld_relaxed(A.ready_in + t) : -1;
-    };
-    // once the input is final (the previous layer completed) every thread
-    // derives validity from the count itself: no polls, fences or barrier
-    int mf = -1;
-    if (XL) {
-      if (ptid == kRes) {
-        // every counter read issued before the first use: one round trip
-        const uint32_t c0 = ld_relaxed_u(A.cnt_in);
-        int r0[kMetaAhead];
-#pragma unroll
-        for (int j = 0; j < kMetaAhead; j++) {
-          const int t = tile_of(item_of(j));
-          r0[j] = (A.ready_in && (int64_t)(t + 1) * T <= A.ld) ? ld_relaxed(A.ready_in + t) : -1;
-        }
-#pragma unroll
-        for (int j = 0; j < kMetaAhead; j++) s_valid[j] = resolve(tile_of(item_of(j)), r0[j], c0);
-        preload(kMetaAhead);
-        if (m_fin >= 0) s_mfin = m_fin;
-      }
-      pbar();
-      mf = s_mfin;
-      if (mf >= 0) {  // input final: the classic bounds from here on
-        M = mf;
-        items = (int)((M + T - 1) / T) * nb;
-      }
-      fence_proxy_async();
-      for (int j = 0; j < kMetaAhead; j++) {
-        if (s_valid[j] <= 0) continue;
-        const int t0 = tile_of(item_of(j));
-        const uint32_t e = (uint32_t)__cvta_generic_to_shared(ment(j));
-        if (ptid >= 2 && ptid < 2 + T / 4)
-          cp_async16(e + 32 + 16 * (ptid - 2), A.a_in + t0 * T + 4 * (ptid - 2));
-      }
-      cp_async_commit();
-    } else {
     // the feature columns of the first entries are fetched together with
     // the active count (one round trip): the tile of a statically dealt item
     // is known without M, and a tile inside the a_in allocation is safe to
@@ -900,7 +792,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       cp_async_wait<0>();
       return;
     }
-    }  // classic prologue
     cp_async_wait<0>();
     pbar();
     for (int k = 0;; k++) {
@@ -914,18 +805,8 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
       cp_async_wait<1>();
       pbar();
-      bool was_early = false;  // cross-layer: the input was not final before this barrier
-      if (XL && mf < 0) {
-        was_early = true;
-        mf = s_mfin;  // the resolver writes it before arriving here
-        if (mf >= 0) {  // input final: the classic bounds from here on
-          M = mf;
-          items = (int)((M + T - 1) / T) * nb;
-        }
-        fence_proxy_async();  // the resolver's acquires reach this thread's TMA reads
-      }
       const int item = item_of(k);
-      if ((XL && mf < 0) ? s_valid[k & 7] < 0 : item >= items) {
+      if (item >= items) {
         cp_async_wait<0>();
         if (pw == 0) {
           // end markers in the next nbuf entries; a consumer warp waits at most
@@ -951,7 +832,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const int *ain = en + 8;
       const int *sfp = en + 8 + T;
       // feature columns 32q + lane (q < FPL) of tile t
-      const int valid = (XL && mf < 0) ? s_valid[k & 7] : min(T, M - t * T);
+      const int valid = min(T, M - t * T);
       int src[FPL];
 #pragma unroll
       for (int q = 0; q < FPL; q++) src[q] = 32 * q + lane < valid ? ain[32 * q + lane] : -1;
@@ -1017,7 +898,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         h->ng = ng;
         h->rec_cnt = rec_cnt;
         h->fp_cnt = fp_cnt;
-        if (XL) h->nst = nst | (valid << 16);
 #ifdef SPDNN_PROFILE
         s_tpost[slot] = clock64();
 #endif
@@ -1066,28 +946,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       // (staged rows; its descriptor landed with this iteration's wait):
       // ring entry k's slot is reused by k + kMetaRing > k + kMetaAhead only.
       // Issued after the header went out: off the slot turnaround path.
-      int v_ahead = 1;
-      bool ain_now = true;
-      if (XL) {
-        // item k+kMetaAhead-1 was resolved in the previous iteration, before
-        // this iteration's barrier: while the input is not final its feature
-        // columns are fetched one iteration late (no extra barrier)
-        if ((mf < 0 || was_early) && s_valid[(k + kMetaAhead - 1) & 7] > 0)
-          prefetch_desc(k + kMetaAhead - 1, false, true);
-        if (mf < 0) {
-          if (ptid == kRes) {
-            s_valid[(k + kMetaAhead) & 7] = resolve(tile_of(item_of(k + kMetaAhead)), pre, pre_c);
-            preload(k + kMetaAhead + 1);  // claimed at the top of this iteration
-            if (m_fin >= 0) s_mfin = m_fin;
-          }
-          ain_now = false;
-        } else {
-          const int ta = tile_of(item_of(k + kMetaAhead));
-          v_ahead = ta * T < mf ? min(T, mf - ta * T) : -1;
-          if (ptid == kRes) s_valid[(k + kMetaAhead) & 7] = v_ahead;
-        }
-      }
-      prefetch_desc(k + kMetaAhead, true, ain_now && v_ahead > 0);
+      prefetch_desc(k + kMetaAhead, true, true);
       prefetch_fp(k + kFpAhead);
       cp_async_commit();
       PROF_MARK(5);  // [5] header
@@ -1104,29 +963,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     // the bits into the tile's word, count the tile's finished blocks, and
     // the item that completes tile t appends the tile's survivors to
     // a_out / cat_out (pruning without a pass over Y).
-    // Cross-layer mode: a finished tile's survivors are announced to the next
-    // layer (per next-layer tile) and the tile counted complete once the
-    // stores are fenced -- at the top of the next iteration, where the
-    // publisher would otherwise wait for the next entry, so the fence does
-    // not sit between an entry's completion and its slot release.
-    // The counter reaching kBig is the next layer's "input final".
-    int pend_base = 0, pend_tot = -1;
-    auto publish = [&]() {
-      if (!XL || pend_tot < 0) return;
-      fence_acq_rel();  // every lane: its a_out / cat_out stores first
-      __syncwarp();
-      if (lane == 0) {
-        for (int p = pend_base, e = pend_base + pend_tot; p < e;) {
-          const int tt = p / T, n = min(e, (tt + 1) * T) - p;
-          red_add_release(A.ready_out + tt, n);
-          p += n;
-        }
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.cnt_out) : "memory");
-      }
-      pend_tot = -1;
-    };
     for (int k = 0;; k++) {
-      publish();  // the tile the previous entry completed, before waiting for this one
       const int slot = k % nbuf;
       const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
       mbar_wait(full0 + 8 * slot, phase);
@@ -1173,16 +1010,11 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last) {
-        if (XL) {  // reset with atomics: the set is reused two launches later
-          if (lane < FPL) wv = atomicExch(&A.tile_alive[FPL * t + lane], 0u);
-          if (lane == 0) atomicExch(&A.tile_done[t], 0);
-        } else {
-          if (lane < FPL) {
-            wv = atomicOr(&A.tile_alive[FPL * t + lane], 0u);
-            A.tile_alive[FPL * t + lane] = 0u;
-          }
-          if (lane == 0) A.tile_done[t] = 0;
+        if (lane < FPL) {
+          wv = atomicOr(&A.tile_alive[FPL * t + lane], 0u);
+          A.tile_alive[FPL * t + lane] = 0u;
         }
+        if (lane == 0) A.tile_done[t] = 0;
         uint32_t mw[FPL];
         int tot = 0, below = 0;
 #pragma unroll
@@ -1201,18 +1033,12 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
           if ((mw[q] >> lane) & 1u) {
             const int j = t * T + FPL * lane + q;
             A.a_out[rank] = j;
-            // (cross-layer: written by another SM's publisher, read past L1)
-            A.cat_out[rank] = XL ? __ldcg(A.cat_in + j) : A.cat_in[j];
+            A.cat_out[rank] = A.cat_in[j];
             rank++;
           }
         }
-        if (XL) {  // signalled after the next slot release (publish below)
-          pend_base = base;
-          pend_tot = tot;
-        }
       }
     }
-    publish();
     return;
   }
 
@@ -1271,10 +1097,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         accumulate<R, FMA, FPL, 4>(acc, recs + (int64_t)meta[seg_base + 2 * g] * RW,
                                    meta[seg_base + 2 * g + 1], ybase, negz2);
       }
-      // the features of the tile that exist end at Mt
-      const int Mt = XL ? h.t * T + (h.nst >> 16) : M;
-      if ((XL ? (h.nst & 0xffff) : h.nst) > 1)
-        accumulate_global<R, FMA, FPL, MASK>(A, acc, h.b, h.t, lane, Mt, negz2);
+      if (h.nst > 1) accumulate_global<R, FMA, FPL, MASK>(A, acc, h.b, h.t, lane, M, negz2);
       PROF_MARK(1);  // [1] record loop
       // output rows and their biases (staged with the block metadata) are read
       // only now, so they hold no registers across the record loop
@@ -1288,7 +1111,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         rows[r] = mrows[r];
         bias[r] = mbias[r];
       }
-      epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, Mt,
+      epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M,
                             reinterpret_cast<uint8_t *>(smem + A.act_off) + (slot * gpi + g) * 32);
       PROF_MARK(2);  // [2] epilogue
     }
@@ -1313,28 +1136,23 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
 
 // ---- launch configuration ---------------------------------------------------
 
-template <int R, int FPL, bool MASK, bool XL>
+template <int R, int FPL, bool MASK>
 void *kernel_ptr(bool fma) {
-  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true, FPL, MASK, XL>)
-             : reinterpret_cast<void *>(&layer_kernel<R, false, FPL, MASK, XL>);
+  return fma ? reinterpret_cast<void *>(&layer_kernel<R, true, FPL, MASK>)
+             : reinterpret_cast<void *>(&layer_kernel<R, false, FPL, MASK>);
 }
 
-template <int FPL, bool MASK, bool XL>
-void *kernel_for_xl(int R, bool fma) {
+template <int FPL, bool MASK>
+void *kernel_for(int R, bool fma) {
   switch (R) {
-    case 1: return kernel_ptr<1, FPL, MASK, XL>(fma);
-    case 3: return kernel_ptr<3, FPL, MASK, XL>(fma);
-    case 6: return kernel_ptr<6, FPL, MASK, XL>(fma);
-    case 7: return kernel_ptr<7, FPL, MASK, XL>(fma);
+    case 1: return kernel_ptr<1, FPL, MASK>(fma);
+    case 3: return kernel_ptr<3, FPL, MASK>(fma);
+    case 4: return kernel_ptr<4, FPL, MASK>(fma);
+    case 5: return kernel_ptr<5, FPL, MASK>(fma);
+    case 6: return kernel_ptr<6, FPL, MASK>(fma);
+    case 7: return kernel_ptr<7, FPL, MASK>(fma);
     default: return nullptr;
   }
-}
-
-// the cross-layer instantiations exist for 128-feature items (FPL = 4) only
-template <int FPL, bool MASK>
-void *kernel_for(int R, bool fma, bool xl) {
-  if (FPL == 4 && xl) return kernel_for_xl<4, MASK, true>(R, fma);
-  return kernel_for_xl<FPL, MASK, false>(R, fma);
 }
 
 struct DevInfo {
@@ -1375,8 +1193,8 @@ template <int FPL, bool MASK>
 int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   using G = Geo<FPL, MASK>;
   const spdnn_layer_dev &L = A.L;
-  void *fn = kernel_for<FPL, MASK>(L.rows_per_group, fma, A.xl != 0);
-  if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1, 3, 6 or 7");
+  void *fn = kernel_for<FPL, MASK>(L.rows_per_group, fma);
+  if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1 or 3..7");
   if (MASK != (L.uniform != 0) || (MASK && L.record_words != 1))
     return spdnn_fail(SPDNN_EINVAL, "layer: record format does not match the layout");
   int sms;
@@ -1558,22 +1376,10 @@ int tensor_map_for(const float *y, int64_t n, int64_t ld, int box_cols, CUtensor
   return rc;
 }
 
-// Cross-layer links of one launch (infer_layers with the scratch's xl buffers).
-struct XlLink {
-  int32_t *tile_done;
-  uint32_t *tile_alive;
-  const int32_t *ready_in;
-  int32_t *ready_out;
-  const uint32_t *cnt_in;
-  uint32_t *cnt_out, *added;
-  bool pdl;
-};
-
 int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, float *y_out,
             int64_t ld, const int32_t *a_in, const int64_t *cat_in, const int32_t *m_in,
             int32_t *a_out, int64_t *cat_out, int32_t *m_out, const spdnn_scratch *scratch,
-            int32_t *work, const spdnn_run_opts *opts, void *stream,
-            const XlLink *xl = nullptr) {
+            int32_t *work, const spdnn_run_opts *opts, void *stream) {
   // ld * 4 must fit 32 bits: the epilogue forms row addresses with one wide multiply
   if (!layer || !bias || !y_in || !y_out || !a_in || !cat_in || !m_in || !a_out ||
       !cat_out || !m_out || !scratch || !work || ld < 1 || ld % SPDNN_TILE_FEATURES ||
@@ -1608,18 +1414,7 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   std::memcpy(&tb, &A.tiny, 4);
   A.tiny_bits_m1 = tb ? tb - 1u : 0u;
   A.negz = -0.0f;
-  bool pdl = kUsePdl != 0;
-  if (xl) {
-    A.xl = 1;
-    A.tile_done = xl->tile_done;
-    A.tile_alive = xl->tile_alive;
-    A.ready_in = xl->ready_in;
-    A.ready_out = xl->ready_out;
-    A.cnt_in = xl->cnt_in;
-    A.cnt_out = xl->cnt_out;
-    A.added = xl->added;
-    pdl = xl->pdl;
-  }
+  const bool pdl = kUsePdl != 0;
   const bool mask = layer->uniform != 0;
   cudaStream_t st = (cudaStream_t)stream;
   if (fpl == 2)
@@ -1646,40 +1441,15 @@ static int infer_layers(int64_t num_layers, const spdnn_layer_dev *layers, const
                         void *const *events) {
   if (num_layers < 0 || (num_layers > 0 && (!layers || !scratch)))
     return spdnn_fail(SPDNN_EINVAL, "spdnn_infer_layers: bad argument");
-  // cross-layer mode: every layer launches (no empty layout) and all the
-  // optional buffers are there
-  bool xl = scratch->y2 && scratch->a2 && scratch->cat2 && scratch->tile_done2 &&
-            scratch->tile_alive2 && scratch->ready && scratch->sync;
-  for (int64_t l = 0; xl && l < num_layers; l++) xl = layers[l].num_blocks > 0;
-  if (opts && opts->features_per_lane == 2) xl = false;  // no FPL = 2 instantiation
-  float *y[3] = {y0, y1, scratch->y2};
-  int32_t *a[3] = {a0, a1, scratch->a2};
-  int64_t *cat[3] = {cat0, cat1, scratch->cat2};
-  const int64_t tc = ld / 64;  // ready counters per layer (64-feature tiles at most)
   for (int64_t l = 0; l < num_layers; l++) {
-    const int nbufs = xl ? 3 : 2;
-    const int i = (int)(l % nbufs), o = (int)((l + 1) % nbufs);
+    const int i = (int)(l & 1), o = i ^ 1;
+    float *y[2] = {y0, y1};
+    int32_t *a[2] = {a0, a1};
+    int64_t *cat[2] = {cat0, cat1};
     if (events && cudaEventRecord((cudaEvent_t)events[l], (cudaStream_t)stream) != cudaSuccess)
       return spdnn_fail(SPDNN_ECUDA, "spdnn_infer_layers_timed: event record failed");
-    XlLink link;
-    if (xl) {
-      // the first layer waits for everything before it (stream order, no
-      // PDL); later ones only for the tiles they read. At most two layers
-      // are resident (every CTA fills an SM), so two tile sets alternate.
-      link.tile_done = (l & 1) ? scratch->tile_done2 : scratch->tile_done;
-      link.tile_alive = (l & 1) ? scratch->tile_alive2 : scratch->tile_alive;
-      link.ready_in = l ? scratch->ready + l * tc : nullptr;
-      link.ready_out = scratch->ready + (l + 1) * tc;
-      // sync = [cnt_0 .. cnt_L][added_0 .. added_L]: cnt_0 = kBig (set by the
-      // caller: the first layer's input is final), cnt_{l+1} = layer l's
-      link.cnt_in = scratch->sync + l;
-      link.cnt_out = scratch->sync + l + 1;
-      link.added = scratch->sync + (num_layers + 1) + l;
-      link.pdl = l > 0;
-    }
     int rc = forward(&layers[l], bias, y[i], y[o], ld, a[i], cat[i], counts + l, a[o], cat[o],
-                     counts + l + 1, scratch, scratch->work + l, opts, stream,
-                     xl ? &link : nullptr);
+                     counts + l + 1, scratch, scratch->work + l, opts, stream);
     if (rc) return rc;
   }
   if (events && cudaEventRecord((cudaEvent_t)events[num_layers], (cudaStream_t)stream) !=

@@ -381,9 +381,8 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
   spdnn_plan_params p = *params;
   if (p.footprint_cap < 1 || p.max_groups < 1 || p.record_cap < p.footprint_cap)
     return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: bad params");
-  if (p.rows_per_group != 0 && p.rows_per_group != 1 && p.rows_per_group != 3 &&
-      p.rows_per_group != 6 && p.rows_per_group != 7)
-    return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: rows_per_group must be 0, 1, 3, 6 or 7");
+  if (p.rows_per_group < 0 || p.rows_per_group == 2 || p.rows_per_group > 7)
+    return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: rows_per_group must be 0, 1 or 3..7");
   if (n > 0 && !valid_csr(n, row_ptr, col_idx))
     return spdnn_fail(SPDNN_EINVAL, "spdnn_plan_build: CSR is not canonical");
   if ((int64_t)p.footprint_cap * SPDNN_STAGED_ROW_BYTES >= (int64_t)1 << 31)

@@ -86,11 +86,28 @@ OPTIMIZED_PARAMS = PlanParams()
 
 @dataclass(frozen=True)
 class PaddingStats:
-    """Union-padding cost of the layout: multiply-add slots vs nonzeros."""
+    """Zero-padding cost of the layout (the reference's fields,
+    spdnn/preprocess.py:115-131), measured on the row-grouped union layout:
+    multiply-add slots executed per feature beyond the nonzeros if record
+    runs were fixed per row group (what the layout stores: one consumer
+    warp's unit), per block, or per layer. Overheads are padded slots / nnz."""
     nnz: int
-    padded_slots: int      # records * R (slots executed per feature)
-    overhead: float        # (padded_slots - nnz) / nnz
+    warp_padded_slots: int
+    tile_padded_slots: int
+    layer_padded_slots: int
+    warp_overhead: float
+    tile_overhead: float
+    layer_overhead: float
     empty: bool = False
+
+    @property
+    def padded_slots(self) -> int:
+        """Slots executed per feature: nnz + the group-level padding."""
+        return self.nnz + self.warp_padded_slots
+
+    @property
+    def overhead(self) -> float:
+        return self.warp_overhead
 
 
 @dataclass(frozen=True)
@@ -162,11 +179,38 @@ def _export(handle) -> LayerPlan:
                      weight_bits=int(s.weight_bits), **arrs)
 
 
+def _group_records(plan: LayerPlan) -> tuple:
+    """(records of every row group, groups of every block) from the exported
+    layout: a block's group segments follow its staged-row list in meta; a
+    multi-stage block (one group) adds its extra stages' records."""
+    blk = plan.blocks.reshape(-1, 8).astype(np.int64)
+    if blk.shape[0] == 0:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64)
+    ng = blk[:, 1]
+    seg = blk[:, 4] + ((blk[:, 5] + 3) & ~3)
+    first = np.repeat(seg - 2 * (np.cumsum(ng) - ng), ng) + 2 * np.arange(int(ng.sum()))
+    recs = plan.meta[first + 1].astype(np.int64)
+    multi = np.nonzero(blk[:, 2] > 1)[0]
+    if len(multi):
+        st = plan.stages.reshape(-1, 4).astype(np.int64)
+        g0 = np.cumsum(ng) - ng
+        for b in multi:
+            e0 = int(blk[b, 3])
+            recs[g0[b]] += int(st[e0: e0 + int(blk[b, 2]) - 1, 3].sum())
+    return recs, ng
+
+
 def _padding(layer: LayerCSR, plan: LayerPlan) -> PaddingStats:
     nnz = layer.nnz
     if nnz == 0:
-        return PaddingStats(0, plan.total_slots, 0.0, empty=True)
-    return PaddingStats(nnz, plan.total_slots, (plan.total_slots - nnz) / nnz)
+        return PaddingStats(0, 0, 0, 0, 0.0, 0.0, 0.0, empty=True)
+    R = plan.rows_per_group
+    recs, ng = _group_records(plan)
+    warp = int(recs.sum()) * R - nnz
+    starts = np.cumsum(ng) - ng
+    tile = int((np.maximum.reduceat(recs, starts) * ng).sum()) * R - nnz if len(recs) else -nnz
+    layer_ = int(recs.max(initial=0)) * len(recs) * R - nnz
+    return PaddingStats(nnz, warp, tile, layer_, warp / nnz, tile / nnz, layer_ / nnz)
 
 
 def build_plans(layers: Sequence[LayerCSR], params: PlanParams, threads: int = 0) -> list:
@@ -183,6 +227,16 @@ def build_plans(layers: Sequence[LayerCSR], params: PlanParams, threads: int = 0
     for i, lay in enumerate(layers):
         if lay.neurons != n:
             raise ModelError("all layers must have the same neuron count")
+        # the C++ builder trusts nnz = row_ptr[n]: the arrays must hold that many
+        rp = np.asarray(lay.row_ptr)
+        if rp.dtype != np.int64 or rp.shape != (n + 1,) or int(rp[0]) != 0 or \
+                np.asarray(lay.col_idx).dtype != np.int32 or \
+                np.asarray(lay.values).dtype != np.float32 or \
+                not len(lay.col_idx) == len(lay.values) == int(rp[-1]) or \
+                not (rp.flags.c_contiguous and lay.col_idx.flags.c_contiguous and
+                     lay.values.flags.c_contiguous):
+            raise ModelError(f"layer {i}: malformed CSR (row_ptr[-1] must equal the "
+                             "col_idx and values lengths)")
         keep.append(lay)
         rps[i] = lay.row_ptr.ctypes.data
         cis[i] = lay.col_idx.ctypes.data if lay.nnz else 0
@@ -374,9 +428,6 @@ class DeviceNetwork:
 
     def _finish(self) -> None:
         self.layer_devs = (_native.LayerDev * max(1, self.num_layers))()
-        # every layer launches a grid (no empty layout): the cross-layer path applies
-        self.launches_every_layer = self.num_layers > 0 and all(
-            pl.num_blocks > 0 for pl in self._plans_meta)
         for l, pl in enumerate(self._plans_meta):
             d = self.layer_devs[l]
             for k in _KINDS:
@@ -406,19 +457,10 @@ class DeviceNetwork:
         self.huge = float(np.ldexp(1.0, min(127, 95 - emax))) if emax < 95 else 0.0
 
 
-# Cross-layer overlap (spdnn_scratch's optional buffers): a layer starts on the
-# input tiles the previous one has published instead of waiting for its whole
-# grid. Opt-in (SPDNN_XL=1): measured on C2 it trims the per-inference fixed
-# cost but costs ~3 % per item, a net loss so far.
-CROSS_LAYER = __import__("os").environ.get("SPDNN_XL", "0") == "1"
-
-
 class Workspace:
     """Per-inference device buffers for a feature-count capacity (reused)."""
 
-    def __init__(self, neurons: int, m_cap: int, num_layers: int, device, buffers: int = 2,
-                 xl: bool = False):
-        buffers = max(buffers, 3) if xl else buffers
+    def __init__(self, neurons: int, m_cap: int, num_layers: int, device, buffers: int = 2):
         torch = _torch()
         self.neurons = neurons
         self.m_cap = m_cap
@@ -437,21 +479,10 @@ class Workspace:
         self.guard = torch.zeros(1, dtype=i32, device=device)
         self.scratch = _native.Scratch(self.tile_done.data_ptr(), self.tile_alive.data_ptr(),
                                        self.work.data_ptr(), self.guard.data_ptr())
-        self.xl = xl
-        if xl:
-            self.tile_done2 = torch.zeros_like(self.tile_done)
-            self.tile_alive2 = torch.zeros_like(self.tile_alive)
-            self.ready = torch.zeros((num_layers + 1) * (self.ld // 64), dtype=i32, device=device)
-            self.sync = torch.zeros(2 * (num_layers + 1), dtype=i32, device=device)
-            for f, t in (("y2", self.y[2]), ("a2", self.a[2]), ("cat2", self.cat[2]),
-                         ("tile_done2", self.tile_done2), ("tile_alive2", self.tile_alive2),
-                         ("ready", self.ready), ("sync", self.sync)):
-                setattr(self.scratch, f, t.data_ptr())
         self.iota = torch.arange(self.ld, dtype=i32, device=device)
 
-    def fits(self, neurons: int, m: int, num_layers: int, xl: bool = False) -> bool:
-        return (neurons == self.neurons and m <= self.m_cap and num_layers <= self.num_layers
-                and xl == self.xl)
+    def fits(self, neurons: int, m: int, num_layers: int) -> bool:
+        return neurons == self.neurons and m <= self.m_cap and num_layers <= self.num_layers
 
 
 _cache_lock = threading.Lock()
@@ -482,12 +513,11 @@ def workspace(neurons: int, m: int, num_layers: int) -> Workspace:
     key = (dev, threading.get_ident())
     with _cache_lock:
         ws = _ws_cache.get(key)
-        if ws is None or not ws.fits(neurons, m, num_layers, CROSS_LAYER):
+        if ws is None or not ws.fits(neurons, m, num_layers):
             ws = None
             _ws_cache.pop(key, None)
             torch.cuda.empty_cache()
-            ws = Workspace(neurons, max(m, 1), num_layers, torch.device("cuda", dev),
-                           xl=CROSS_LAYER)
+            ws = Workspace(neurons, max(m, 1), num_layers, torch.device("cuda", dev))
             _ws_cache[key] = ws
         return ws
 
@@ -498,11 +528,11 @@ def workspace(neurons: int, m: int, num_layers: int) -> Workspace:
 class DeviceRun:
     """State of one on-device inference after the layer loop."""
 
-    def __init__(self, ws: Workspace, num_layers: int, m0: int, nbufs: int = 2):
+    def __init__(self, ws: Workspace, num_layers: int, m0: int):
         self.ws = ws
         self.num_layers = num_layers
         self.m0 = m0
-        self.out_index = num_layers % nbufs
+        self.out_index = num_layers % 2
         self.fma = False
         self.guard = 0  # filled by collect(): bit 0 FMA-form guard, bit 1 non-finite input
 
@@ -540,36 +570,29 @@ FEATURES_PER_LANE = int(__import__("os").environ.get("SPDNN_FEATURES_PER_LANE", 
 
 def run_opts(net: DeviceNetwork, fma: bool | None = None) -> _native.RunOpts:
     use = net.pow2 if fma is None else (fma and net.pow2)
+    if FEATURES_PER_LANE not in (2, 4):
+        raise ModelError(f"SPDNN_FEATURES_PER_LANE must be 2 or 4, not {FEATURES_PER_LANE}")
     return _native.RunOpts(int(use), net.tiny, FEATURES_PER_LANE)
 
 
-def reset_run(net: DeviceNetwork, ws: Workspace, m0: int) -> bool:
-    """Zero the per-run counters (stream-ordered); True when the run takes the
-    cross-layer path (final state in buffer num_layers % 3)."""
+def reset_run(ws: Workspace, m0: int) -> None:
+    """Zero the per-run counters (stream-ordered)."""
     ws.counts.zero_()
     ws.counts[0] = m0
     ws.work.zero_()
-    # the cross-layer path needs every layer to launch (the C side falls back
-    # to the two-buffer path otherwise, and so must the output index)
-    xl = ws.xl and net.launches_every_layer and FEATURES_PER_LANE == 4
-    if xl:
-        ws.ready.zero_()
-        ws.sync.zero_()
-        ws.sync[0] = 1 << 30  # completion counter "before" the first layer: its input is final
-    return xl
 
 
 def run_layers(net: DeviceNetwork, ws: Workspace, m0: int, fma: bool | None = None
                ) -> DeviceRun:
     """Enqueue every layer on the current stream; no host synchronisation."""
     torch = _torch()
-    xl = reset_run(net, ws, m0)
+    reset_run(ws, m0)
     opts = run_opts(net, fma)
     _native.check(_native.lib().spdnn_infer_layers(
         net.num_layers, net.layer_devs, _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
         _dptr(ws.a[0]), _dptr(ws.a[1]), _dptr(ws.cat[0]), _dptr(ws.cat[1]), _dptr(ws.counts),
         ctypes.byref(ws.scratch), ctypes.byref(opts), _stream_ptr(torch)), "spdnn_infer_layers")
-    run = DeviceRun(ws, net.num_layers, m0, 3 if xl else 2)
+    run = DeviceRun(ws, net.num_layers, m0)
     run.fma = bool(opts.fma_form)
     return run
 
@@ -1078,6 +1101,11 @@ def optimized_layer(features: FeatureBatch, prepared, bias: np.ndarray,
     """
     if minibatch is not None and minibatch < 1:
         raise ModelError("minibatch must be positive")
+    if hasattr(prepared, "wdispl") and hasattr(prepared, "windex"):
+        # a layer prepared by the reference itself (its sliced ELL): same
+        # weights, laid out for this kernel
+        csr = csr_from_sliced_ell(prepared)
+        prepared = PreparedLayer(csr=csr, plan=build_plans([csr], OPTIMIZED_PARAMS)[0])
     if isinstance(prepared, LayerPlan):
         prepared = PreparedLayer(csr=None, plan=prepared)
     if prepared.plan is None:
@@ -1086,6 +1114,30 @@ def optimized_layer(features: FeatureBatch, prepared, bias: np.ndarray,
     if features.neurons != n or len(bias) != n:
         raise ModelError("dimension mismatch in optimized_layer")
     return _one_layer(features, prepared, np.asarray(bias, np.float32))
+
+
+def csr_from_sliced_ell(ell) -> LayerCSR:
+    """The CSR layer behind a reference-prepared sliced-ELL layer
+    (spdnn/preprocess.py:86-113 documents the format: slice m of warp slot
+    w = stage * warps_per_block + warp holds one entry per lane; the lane's
+    row is block * block_size + warp * warp_size + lane, the entry's column
+    plan.map[mapdispl[stage] + windex]; padding has value 0)."""
+    from .model import make_layer_csr
+    plan, ws = ell.plan, int(ell.warp_size)
+    wpb = int(plan.block_size) // ws
+    wdispl = np.asarray(ell.wdispl, np.int64)
+    n_slices = int(wdispl[-1]) if len(wdispl) else 0
+    idx = np.arange(n_slices * ws, dtype=np.int64)
+    m, lane = idx // ws, idx % ws
+    wslot = np.searchsorted(wdispl, m, side="right") - 1
+    stage, warp = wslot // wpb, wslot % wpb
+    block = np.searchsorted(np.asarray(plan.buffdispl, np.int64), stage, side="right") - 1
+    rows = block * int(plan.block_size) + warp * ws + lane
+    vals = np.asarray(ell.wvalue, np.float32)[:n_slices * ws]
+    cols = np.asarray(plan.map, np.int64)[np.asarray(plan.mapdispl, np.int64)[stage] +
+                                          np.asarray(ell.windex, np.int64)[:n_slices * ws]]
+    keep = vals != 0
+    return make_layer_csr(int(ell.neurons), rows[keep], cols[keep], vals[keep])
 
 
 def baseline_layer(features: FeatureBatch, layer: LayerCSR, bias: np.ndarray):

@@ -399,19 +399,21 @@ class DeviceShard:
 
     def take_top(self, k: int):
         """Remove the k highest-category active features; returns their values
-        ((k, N) feature-major) and categories, highest last."""
+        ((k, N) feature-major) and categories, highest last. Device-side only
+        (a stable sort and gathers, no host synchronisation); the kept
+        features keep their relative order."""
         torch = self.engine._torch()
         ws, c = self.ws, self.cur
         cats = ws.cat[c][: self.m]
-        top = torch.topk(cats, k, largest=True, sorted=True).indices.flip(0)
+        order = torch.argsort(cats, stable=True)
+        top = order[self.m - k:]
+        keep = torch.sort(order[: self.m - k]).values
         vals = torch.empty((k, self.n), dtype=torch.float32, device=cats.device)
         self.engine._native.check(self.engine._native.lib().spdnn_gather_out(
             self.engine._dptr(ws.y[c]), self.n, ws.ld, self.engine._dptr(ws.a[c]),
             self.engine._dptr(top), k, self.engine._dptr(vals),
             self.engine._stream_ptr(torch)), "spdnn_gather_out")
-        sent_cats = cats[top].clone()
-        keep = torch.ones(self.m, dtype=torch.bool, device=cats.device)
-        keep[top] = False
+        sent_cats = cats[top]
         a_keep, c_keep = ws.a[c][: self.m][keep], cats[keep]
         self.m -= k
         ws.a[c][: self.m].copy_(a_keep)
@@ -485,8 +487,8 @@ class LocalTransport:
         self.local = list(range(workers))
         self.root = True
 
-    def allgather_counts(self, layer: int, mine: dict) -> list:
-        if self.hook is not None:
+    def allgather_counts(self, layer: int, mine: dict, notify: bool = True) -> list:
+        if self.hook is not None and notify:
             for w in self.local:
                 for other in range(self.workers):
                     if other != w:
@@ -552,12 +554,16 @@ class DistTransport:
         return torch.empty(shape, dtype=dtype,
                            device=self.device if self.wire is not None else "cpu")
 
-    def allgather_counts(self, layer: int, mine: dict) -> list:
+    def allgather_counts(self, layer: int, mine: dict, notify: bool = True) -> list:
+        """One count per rank to every rank (NCCL allgather on GPUs, gloo on
+        CPU). `notify` = False for the exchanges the reference has no message
+        for (the initial counts, the gather sizes): the latency hook sees the
+        reference's message stream only (parallel.py:306-318)."""
         import torch
         t = self._wire(torch.tensor([mine[self.rank]], dtype=torch.int64, device=self.device))
         out = [self._empty(1, torch.int64) for _ in range(self.workers)]
-        self.dist.all_gather(out, t)  # NCCL allgather on GPUs (gloo on CPU)
-        if self.hook is not None:
+        self.dist.all_gather(out, t)
+        if self.hook is not None and notify:
             for other in range(self.workers):
                 if other != self.rank:
                     self.hook(CountMsg(src=self.rank, layer=layer, count=mine[self.rank]))
@@ -607,21 +613,38 @@ class DistTransport:
             me.append(vals, cats)
 
     def gather(self, shards: dict, values: bool):
-        """Every rank gets every worker's (categories, values)."""
+        """Algorithm 2's final step (parallel.py:417-433): every
+        worker sends its survivors' categories (and values when asked) to
+        rank 0, which merges them. Rank 0 returns every worker's part; the
+        other ranks return their own part only."""
         import torch
         cats, vals = shards[self.rank].final(values)
-        counts = self.allgather_counts(-1, {self.rank: int(cats.shape[0])})
+        counts = self.allgather_counts(-1, {self.rank: int(cats.shape[0])}, notify=False)
         n = shards[self.rank].n
-        parts = []
-        for w in range(self.workers):
-            c = self._wire(cats) if w == self.rank else self._empty(counts[w], torch.int64)
-            self.dist.broadcast(c, src=w)
-            v = None
-            if values:
-                v = self._wire(vals) if w == self.rank else self._empty((counts[w], n),
-                                                                         torch.float32)
-                self.dist.broadcast(v, src=w)
+        if self.rank != 0:
+            if self.hook is not None:
+                self.hook(GatherMsg(src=self.rank, data=vals, categories=cats))
+            ops = []
+            if counts[self.rank]:
+                ops.append(self.dist.P2POp(self.dist.isend, self._wire(cats.contiguous()), 0))
+                if values:
+                    ops.append(self.dist.P2POp(self.dist.isend, self._wire(vals.contiguous()), 0))
+            if ops:
+                for req in self.dist.batch_isend_irecv(ops):
+                    req.wait()
+            return [(cats, vals)]
+        parts, ops = [(cats, vals)], []
+        for w in range(1, self.workers):
+            c = self._empty(counts[w], torch.int64)
+            v = self._empty((counts[w], n), torch.float32) if values else None
+            if counts[w]:
+                ops.append(self.dist.P2POp(self.dist.irecv, c, w))
+                if values:
+                    ops.append(self.dist.P2POp(self.dist.irecv, v, w))
             parts.append((c, v))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
         return parts
 
 
@@ -661,7 +684,7 @@ def run_layers_parallel(num_layers: int, shards: dict, transport, threshold: flo
     totals = []
     hook = transport.hook
     local = transport.local
-    before = sum(transport.allgather_counts(-1, {w: shards[w].m for w in local}))
+    before = sum(transport.allgather_counts(-1, {w: shards[w].m for w in local}, notify=False))
     k_max = max(1, window or WINDOW_MAX)
     k_cur = min(WINDOW_MIN, k_max)
     speculate = SPECULATE and all(getattr(shards[w], "supports_speculation", False)
@@ -759,8 +782,12 @@ def run_batch_parallel(model: NetworkModel, inputs: FeatureBatch, config: Infere
                        mode: str = "optimized", prepared=None,
                        latency_hook: LatencyHook | None = None, values: bool = True):
     """Inference across ``config.workers`` shards with per-layer balancing
-    (parallel.py:379-454). Returns (InferenceResult, CommMatrix, BalanceReport);
-    under torch.distributed every rank returns the same merged result."""
+    (parallel.py:379-454). Returns (InferenceResult, CommMatrix, BalanceReport).
+    Under torch.distributed (one worker per rank) the survivors are gathered
+    to rank 0 (Algorithm 2): rank 0's result holds the merged,
+    sorted categories (and values); every other rank's holds its own shard's
+    survivors. Per-layer counts, CommMatrix and BalanceReport are the same on
+    every rank.""" 
     from . import engine
 
     if inputs.neurons != model.neurons:

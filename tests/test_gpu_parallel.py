@@ -151,10 +151,13 @@ def test_shard_only_two_ranks_chunk_built(cuda_ok):
     inputs = ingest.generate_synthetic_inputs(1024, 900, 0.3, seed=22)
     single = engine.infer(model, inputs, InferenceConfig())
     for rank, cats, per_layer, vbits, edges in res:
-        assert cats == single.categories.tolist()
         assert per_layer == [(o.active_before, o.active_after) for o in single.per_layer]
-        assert vbits == np.asarray(single.final.data).view(np.uint32).tobytes()
         assert edges == single.edges_processed
+        if rank == 0:  # the merged survivors live on rank 0 (Algorithm 2)
+            assert cats == single.categories.tolist()
+            assert vbits == np.asarray(single.final.data).view(np.uint32).tobytes()
+        else:
+            assert set(cats) < set(single.categories.tolist())
 
 
 def _dist_worker(rank, world, port, q):
@@ -201,10 +204,13 @@ def test_distributed_transport_two_ranks(cuda_ok):
     inputs = make_feature_batch(1024, data)
     single = engine.infer(model, inputs, InferenceConfig())
     for rank, cats, per_layer, vsum, moved in res:
-        assert cats == single.categories.tolist()
         assert per_layer == [(o.active_before, o.active_after) for o in single.per_layer]
-        assert vsum == float(np.asarray(single.final.data, np.float64).sum())
-    assert res[0][1:] == res[1][1:]
+        if rank == 0:
+            assert cats == single.categories.tolist()
+            assert vsum == float(np.asarray(single.final.data, np.float64).sum())
+        else:
+            assert set(cats) < set(single.categories.tolist())
+    assert res[0][2] == res[1][2] and res[0][4] == res[1][4]
 
 
 def test_stress_matches_reference_run_batch_parallel(cuda_ok):

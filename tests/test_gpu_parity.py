@@ -48,7 +48,8 @@ PARAMS = [PlanParams(), PlanParams(rows_per_group=1, reorder=False),
           PlanParams(rows_per_group=3), PlanParams(rows_per_group=7, reorder=False),
           PlanParams(rows_per_group=7, footprint_cap=5, record_cap=8, max_groups=3),
           PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2),
-          PlanParams(rows_per_group=6)]
+          PlanParams(rows_per_group=6), PlanParams(rows_per_group=5),
+          PlanParams(rows_per_group=4)]
 
 
 @pytest.mark.parametrize("pi", range(len(PARAMS)))
@@ -470,23 +471,3 @@ def test_randomized_structured_networks(cuda_ok):
         assert [o.active_before for o in res.per_layer] + [len(res.categories)] == \
             ref.counts.tolist(), msg
         assert same_bits(res.final.data, ref.final), msg
-
-
-@pytest.mark.parametrize("case", ["flagship", "config1", "edge", "random", "structured"])
-def test_cross_layer_mode(cuda_ok, monkeypatch, case):
-    """The opt-in cross-layer path (SPDNN_XL=1: a layer starts on the tiles the
-    previous one has published, three rotating buffers, per-tile readiness
-    counters) gives the same bits on the digests, the edge cases (all features
-    dying in layer 0: the completion counters cascade through empty layers),
-    random networks and the structured ones."""
-    monkeypatch.setattr(engine, "CROSS_LAYER", True)
-    if case == "flagship":
-        test_flagship_digest(cuda_ok)
-    elif case == "config1":
-        test_config1_full_digest(cuda_ok)
-    elif case == "edge":
-        test_edge_cases(cuda_ok)
-    elif case == "random":
-        test_infer_random_pm_networks_vs_oracle(cuda_ok)
-    else:
-        test_randomized_structured_networks(cuda_ok)

@@ -22,6 +22,8 @@ PARAMS = [
     PlanParams(rows_per_group=3, footprint_cap=2, record_cap=2, max_groups=16),
     PlanParams(rows_per_group=1, footprint_cap=1, record_cap=1, max_groups=1),
     PlanParams(rows_per_group=6),
+    PlanParams(rows_per_group=5),
+    PlanParams(rows_per_group=4, footprint_cap=9, record_cap=12, max_groups=5),
 ]
 
 
@@ -113,7 +115,9 @@ def test_empty_and_degenerate_layers():
 def test_plan_rejects_bad_params():
     layer = make_layer_csr(4, np.array([0]), np.array([1]), np.array([1.0], np.float32))
     with pytest.raises(ModelError):
-        build_plans([layer], PlanParams(rows_per_group=5))
+        build_plans([layer], PlanParams(rows_per_group=2))
+    with pytest.raises(ModelError):
+        build_plans([layer], PlanParams(rows_per_group=8))
     with pytest.raises(ModelError):
         build_plans([layer], PlanParams(footprint_cap=0))
 
