@@ -140,48 +140,82 @@ def generate_synthetic_inputs(neurons: int, count: int, density: float, seed: in
 
 
 # ---------------------------------------------------------------------------
-# challenge TSV files (spdnn/ingest.py:56-135)
+# challenge TSV files (formats and IngestError cases of spdnn/ingest.py:56-135)
+#
+# Parsing is vectorised: the whole text is decoded once, split into lines
+# (universal newlines, as a text stream reads them), and the well-formed case
+# is converted by numpy's C parser in one call. Only when that fails are the
+# lines scanned one by one, to report the first bad line exactly as the
+# reference does ("parse error, line N: ...").
 
-def _lines(source: Union[bytes, BinaryIO]) -> io.TextIOBase:
-    if isinstance(source, bytes):
-        source = io.BytesIO(source)
-    return io.TextIOWrapper(source, encoding="ascii")
-
-
-def _parse_triplet(line: str, lineno: int) -> tuple:
-    parts = line.split("\t")
-    if len(parts) != 3:
-        raise IngestError(f"parse error, line {lineno}: expected 3 tab-separated fields")
+def _text_lines(source: Union[bytes, BinaryIO]) -> tuple:
+    """(stripped non-blank lines, their 1-based line numbers)."""
+    raw = source if isinstance(source, (bytes, bytearray)) else source.read()
     try:
-        return int(parts[0]), int(parts[1]), float(parts[2])
-    except ValueError:
-        raise IngestError(f"parse error, line {lineno}: bad integer or float") from None
+        text = bytes(raw).decode("ascii")
+    except UnicodeDecodeError as exc:
+        raise IngestError(f"parse error: non-ASCII byte at offset {exc.start}") from None
+    lines = text.replace("\r\n", "\n").replace("\r", "\n").split("\n")
+    keep = [(i + 1, ln.strip()) for i, ln in enumerate(lines) if ln.strip()]
+    return [ln for _, ln in keep], np.array([i for i, _ in keep], dtype=np.int64)
 
 
-def _triplets(source, lo_hi_a, lo_hi_b, what_a: str, what_b: str):
-    """(a-1, b-1, value) arrays of the non-blank lines; 1-based range checks
-    in line order, as the reference does them."""
-    a_s, b_s, v_s = [], [], []
-    for lineno, line in enumerate(_lines(source), start=1):
-        line = line.strip()
-        if not line:
-            continue
-        a, b, v = _parse_triplet(line, lineno)
-        if not 1 <= a <= lo_hi_a:
-            raise IngestError(f"{what_a} index out of range, line {lineno}")
-        if not 1 <= b <= lo_hi_b:
-            raise IngestError(f"{what_b} index out of range, line {lineno}")
-        a_s.append(a - 1)
-        b_s.append(b - 1)
-        v_s.append(v)
-    return (np.array(a_s, dtype=np.int64), np.array(b_s, dtype=np.int64),
-            np.array(v_s, dtype=np.float32))
+def _first_bad_line(lines, linenos, fields: int, kinds: str) -> None:
+    """Raise the reference's message for the first line that does not parse
+    as `fields` tab-separated values of `kinds` ('i' int, 'f' float)."""
+    for ln, no in zip(lines, linenos.tolist()):
+        parts = ln.split("\t") if fields > 1 else [ln]
+        if len(parts) != fields:
+            raise IngestError(f"parse error, line {no}: expected {fields} tab-separated fields")
+        try:
+            for part, kind in zip(parts, kinds):
+                (int if kind == "i" else float)(part)
+        except ValueError:
+            what = "bad integer or float" if fields > 1 else "bad integer"
+            raise IngestError(f"parse error, line {no}: {what}") from None
+
+
+def _columns(lines, linenos, fields: int, kinds: str) -> list:
+    """The lines as `fields` numpy columns (int64 / float64)."""
+    if not lines:
+        return [np.zeros(0, np.int64 if k == "i" else np.float64) for k in kinds]
+    arr = None
+    if all(ln.count("\t") == fields - 1 for ln in lines):
+        dt = [(f"c{j}", "<i8" if k == "i" else "<f8") for j, k in enumerate(kinds)]
+        try:
+            arr = np.loadtxt(io.StringIO("\n".join(lines)), delimiter="\t" if fields > 1 else None,
+                             dtype=dt, ndmin=1, comments=None)
+        except ValueError:
+            arr = None
+    if arr is None or arr.shape[0] != len(lines):
+        _first_bad_line(lines, linenos, fields, kinds)
+        # numpy refused a line Python accepts (e.g. "1_0"): convert per line
+        conv = [[(int if k == "i" else float)(x) for x, k in
+                 zip(ln.split("\t") if fields > 1 else [ln], kinds)] for ln in lines]
+        return [np.array([c[j] for c in conv], np.int64 if k == "i" else np.float64)
+                for j, k in enumerate(kinds)]
+    return [arr[f"c{j}"] for j in range(fields)]
+
+
+def _checked_triplets(source, hi_a: int, hi_b: int, what_a: str, what_b: str):
+    """(a - 1, b - 1, value) of the non-blank lines; 1-based range checks,
+    the first offending line (in line order) reported as the reference does."""
+    lines, linenos = _text_lines(source)
+    a, b, v = _columns(lines, linenos, 3, "iif")
+    bad_a = (a < 1) | (a > hi_a)
+    bad_b = (b < 1) | (b > hi_b)
+    bad = bad_a | bad_b
+    if bad.any():
+        j = int(np.argmax(bad))
+        what = what_a if bad_a[j] else what_b
+        raise IngestError(f"{what} index out of range, line {int(linenos[j])}")
+    return a - 1, b - 1, v.astype(np.float32)
 
 
 def load_layer_tsv(source: Union[bytes, BinaryIO], neurons: int) -> LayerCSR:
     """One weight layer from ``row<TAB>col<TAB>value`` lines (1-indexed); line
     order is free, a repeated (row, col) is an error (ingest.py:67-90)."""
-    rows, cols, vals = _triplets(source, neurons, neurons, "row", "column")
+    rows, cols, vals = _checked_triplets(source, neurons, neurons, "row", "column")
     try:
         return make_layer_csr(neurons, rows, cols, vals)
     except ModelError as exc:
@@ -193,7 +227,7 @@ def load_features_tsv(source: Union[bytes, BinaryIO], neurons: int,
     """Features from ``image<TAB>neuron<TAB>value`` lines (1-indexed) into a
     dense (N, max_inputs) Fortran batch; absent images are zero columns and a
     repeated (image, neuron) keeps the last value (ingest.py:93-111)."""
-    img, neu, vals = _triplets(source, max_inputs, neurons, "image", "neuron")
+    img, neu, vals = _checked_triplets(source, max_inputs, neurons, "image", "neuron")
     data = np.zeros((neurons, max_inputs), dtype=np.float32, order="F")
     data[neu, img] = vals  # numpy assigns repeated indices in order: last wins
     return make_feature_batch(neurons, data)
@@ -202,111 +236,118 @@ def load_features_tsv(source: Union[bytes, BinaryIO], neurons: int,
 def load_truth_categories(source: Union[bytes, BinaryIO]) -> list:
     """Sorted 0-based categories from one 1-based integer per line;
     duplicates are rejected (ingest.py:114-132)."""
-    cats = []
-    for lineno, line in enumerate(_lines(source), start=1):
-        line = line.strip()
-        if not line:
-            continue
-        try:
-            cats.append(int(line))
-        except ValueError:
-            raise IngestError(f"parse error, line {lineno}: bad integer") from None
-    cats.sort()
-    for a, b in zip(cats, cats[1:]):
-        if a == b:
-            raise IngestError(f"duplicate category {a}")
-    return [c - 1 for c in cats]
+    lines, linenos = _text_lines(source)
+    (cats,) = _columns(lines, linenos, 1, "i")
+    cats = np.sort(cats)
+    dup = np.nonzero(cats[1:] == cats[:-1])[0]
+    if dup.size:
+        raise IngestError(f"duplicate category {int(cats[dup[0]])}")
+    return (cats - 1).tolist()
 
 
 # ---------------------------------------------------------------------------
-# binary cache (spdnn/ingest.py:182-270), little-endian:
+# binary cache (byte formats of spdnn/ingest.py:182-270), little-endian:
 #   model    "SPDN" | u32 version | u32 N | u32 L | per layer: u64 nnz,
 #            u64 row_ptr[N+1], u32 col_idx[nnz], f32 values[nnz] | f32 bias[N]
 #   features "SPDF" | u32 version | u32 N | u32 M | u64 nnz |
 #            nnz x (u32 image, u32 neuron, f32 value), image-major
 
-_REC = np.dtype([("img", "<u4"), ("neu", "<u4"), ("val", "<f4")])
+_FEATURE_RECORD = np.dtype([("img", "<u4"), ("neu", "<u4"), ("val", "<f4")])
 
 
-def _put(out: BinaryIO, arr, dtype: str) -> None:
-    out.write(np.ascontiguousarray(arr).astype(dtype).tobytes())
+def _model_chunks(model: NetworkModel) -> Iterator[bytes]:
+    yield MODEL_MAGIC + np.array([FORMAT_VERSION, model.neurons, model.num_layers],
+                                 "<u4").tobytes()
+    for layer in model.layers:
+        yield np.array([layer.nnz], "<u8").tobytes()
+        yield layer.row_ptr.astype("<u8").tobytes()
+        yield layer.col_idx.astype("<u4").tobytes()
+        yield layer.values.astype("<f4").tobytes()
+    yield np.asarray(model.bias).astype("<f4").tobytes()
+
+
+def _feature_chunks(batch: FeatureBatch) -> Iterator[bytes]:
+    if not np.array_equal(batch.categories, np.arange(batch.total_inputs)):
+        raise IngestError("only full input batches can be cached")
+    dense = np.asarray(batch.data)
+    img, neu = np.nonzero(dense.T)  # image-major: all of image 0's nonzeros first
+    recs = np.empty(img.shape[0], _FEATURE_RECORD)
+    recs["img"], recs["neu"], recs["val"] = img, neu, dense[neu, img]
+    yield FEATURES_MAGIC + np.array([FORMAT_VERSION, batch.neurons, batch.active_count],
+                                    "<u4").tobytes()
+    yield np.array([recs.shape[0]], "<u8").tobytes()
+    yield recs.tobytes()
 
 
 def write_binary(obj: Union[NetworkModel, FeatureBatch], dest: BinaryIO) -> None:
-    """Serialize a model or a full input batch (ingest.py:198-224)."""
+    """Serialize a model or a full input batch (ingest.py:198-224), one
+    section at a time (a 65536 x 1920 model is never concatenated in memory)."""
     if isinstance(obj, NetworkModel):
-        dest.write(MODEL_MAGIC)
-        _put(dest, np.array([FORMAT_VERSION, obj.neurons, obj.num_layers]), "<u4")
-        for layer in obj.layers:
-            _put(dest, np.array([layer.nnz]), "<u8")
-            _put(dest, layer.row_ptr, "<u8")
-            _put(dest, layer.col_idx, "<u4")
-            _put(dest, layer.values, "<f4")
-        _put(dest, obj.bias, "<f4")
+        chunks = _model_chunks(obj)
     elif isinstance(obj, FeatureBatch):
-        if not np.array_equal(obj.categories, np.arange(obj.total_inputs)):
-            raise IngestError("only full input batches can be cached")
-        dest.write(FEATURES_MAGIC)
-        image_idx, neuron_idx = np.nonzero(obj.data.T)  # image-major record order
-        _put(dest, np.array([FORMAT_VERSION, obj.neurons, obj.active_count]), "<u4")
-        _put(dest, np.array([len(image_idx)]), "<u8")
-        rec = np.empty(len(image_idx), dtype=_REC)
-        rec["img"] = image_idx
-        rec["neu"] = neuron_idx
-        rec["val"] = obj.data[neuron_idx, image_idx]
-        dest.write(rec.tobytes())
+        chunks = _feature_chunks(obj)
     else:
         raise TypeError(f"cannot serialize {type(obj).__name__}")
+    for chunk in chunks:
+        dest.write(chunk)
 
 
-class _Reader:
-    def __init__(self, src: BinaryIO):
-        self._src = src
-
-    def take(self, nbytes: int) -> bytes:
-        buf = self._src.read(nbytes)
-        if len(buf) != nbytes:
-            raise IngestError("truncated file")
-        return buf
-
-    def scalar(self, dtype: str) -> int:
-        dt = np.dtype(dtype)
-        return int(np.frombuffer(self.take(dt.itemsize), dtype=dt)[0])
-
-    def array(self, count: int, dtype: str) -> np.ndarray:
-        dt = np.dtype(dtype)
-        return np.frombuffer(self.take(dt.itemsize * count), dtype=dt)
+def _buffer_of(src: BinaryIO) -> memoryview:
+    """The stream's remaining bytes without a copy when it is a regular file
+    (memory-mapped) or an in-memory buffer; otherwise read once."""
+    if isinstance(src, io.BytesIO):
+        return src.getbuffer()[src.tell():]
+    try:
+        import mmap
+        fd = src.fileno()
+        start = src.tell()
+        mm = mmap.mmap(fd, 0, access=mmap.ACCESS_READ)
+        return memoryview(mm)[start:]
+    except (AttributeError, OSError, ValueError, io.UnsupportedOperation):
+        return memoryview(src.read())
 
 
 def read_binary(src: BinaryIO, out: np.ndarray | None = None
                 ) -> Union[NetworkModel, FeatureBatch]:
     """Read back what write_binary produced, dispatching on the magic
-    (ingest.py:242-270). ``out`` (extension, features only): an (N, M)
-    Fortran float32 array to scatter the records into -- e.g. a pinned host
-    buffer, so the batch can be uploaded without another host copy."""
-    rd = _Reader(src)
-    magic = rd.take(4)
-    if magic not in (MODEL_MAGIC, FEATURES_MAGIC):
+    (ingest.py:242-270). The stream is viewed as one buffer (memory-mapped
+    when it is a file) and sliced with np.frombuffer. ``out`` (extension,
+    features only): an (N, M) Fortran float32 array to scatter the records
+    into -- e.g. a pinned host buffer, so the batch can be uploaded without
+    another host copy."""
+    buf = _buffer_of(src)
+    pos = 0
+
+    def take(dtype: str, count: int = 1) -> np.ndarray:
+        nonlocal pos
+        dt = np.dtype(dtype)
+        end = pos + dt.itemsize * count
+        if end > len(buf):
+            raise IngestError("truncated file")
+        arr = np.frombuffer(buf[pos:end], dtype=dt)
+        pos = end
+        return arr
+
+    if len(buf) < 4 or bytes(buf[:4]) not in (MODEL_MAGIC, FEATURES_MAGIC):
         raise IngestError("bad magic")
-    version = rd.scalar("<u4")
+    magic = bytes(buf[:4])
+    pos = 4
+    version = int(take("<u4")[0])
     if version != FORMAT_VERSION:
         raise IngestError(f"unsupported format version {version}")
+    n, count = (int(x) for x in take("<u4", 2))
     if magic == MODEL_MAGIC:
-        n = rd.scalar("<u4")
-        num_layers = rd.scalar("<u4")
         layers = []
-        for _ in range(num_layers):
-            nnz = rd.scalar("<u8")
-            row_ptr = rd.array(n + 1, "<u8").astype(np.int64)
-            col_idx = rd.array(nnz, "<u4").astype(np.int32)
-            values = rd.array(nnz, "<f4").astype(np.float32)
+        for _ in range(count):
+            nnz = int(take("<u8")[0])
+            row_ptr = take("<u8", n + 1).astype(np.int64)
+            col_idx = take("<u4", nnz).astype(np.int32)
+            values = take("<f4", nnz).astype(np.float32)
             layers.append(LayerCSR(row_ptr=row_ptr, col_idx=col_idx, values=values))
-        bias = rd.array(n, "<f4").astype(np.float32)
+        bias = take("<f4", n).astype(np.float32)
         return NetworkModel(neurons=n, layers=tuple(layers), bias=bias)
-    n = rd.scalar("<u4")
-    m = rd.scalar("<u4")
-    nnz = rd.scalar("<u8")
-    rec = np.frombuffer(rd.take(_REC.itemsize * nnz), dtype=_REC)
+    m = count
+    recs = take(_FEATURE_RECORD, int(take("<u8")[0]))
     if out is not None:
         if out.shape != (n, m) or out.dtype != np.float32 or not out.flags.f_contiguous:
             raise IngestError("out must be an (N, M) Fortran float32 array")
@@ -314,7 +355,7 @@ def read_binary(src: BinaryIO, out: np.ndarray | None = None
         data[...] = 0.0
     else:
         data = np.zeros((n, m), dtype=np.float32, order="F")
-    if nnz and (int(rec["neu"].max()) >= n or int(rec["img"].max()) >= m):
+    if recs.size and (int(recs["neu"].max()) >= n or int(recs["img"].max()) >= m):
         raise IngestError("record index out of range")
-    data[rec["neu"], rec["img"]] = rec["val"]
+    data[recs["neu"], recs["img"]] = recs["val"]
     return make_feature_batch(n, data)

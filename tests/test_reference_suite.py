@@ -58,3 +58,31 @@ def test_reference_suite_on_drop_in(cuda_ok, tmp_path):
     failed = sorted(k for k, v in outcomes.items() if v == "failed")
     unexpected = [k for k in failed if k not in allowed]
     assert not unexpected, (unexpected, proc.stdout[-4000:])
+
+
+# reference tests that run the engine (a CUDA device) -- the GPU test above
+# covers them; every other test of these files runs on the CPU here
+_HOST_FILES = ("test_ingest.py", "test_model.py", "test_report.py", "test_preprocess.py",
+               "test_parallel.py", "test_oracle.py")
+_NEEDS_GPU = ("test_parallel.py::test_single_worker_matches_engine",
+              "test_parallel.py::test_worker_count_invariance",
+              "test_parallel.py::test_adversarial_die_off_triggers_rebalance",
+              "test_parallel.py::test_infinite_threshold_disables_rebalancing",
+              "test_parallel.py::test_latency_hook_sees_typed_messages",
+              "test_parallel.py::test_baseline_mode_parallel",
+              "test_parallel.py::test_more_workers_than_features",
+              "test_oracle.py::test_matches_baseline_engine")
+
+
+def test_reference_host_tests_on_drop_in(tmp_path):
+    """The reference's loader, model, report, balancing-rule and oracle tests
+    against the drop-in on the CPU (--noconftest: the reference's conftest
+    warms its engine, which here needs the GPU)."""
+    if not os.path.isdir(REF_TESTS):
+        pytest.skip("baseline/_ref/tests missing (tools/install_reference.sh)")
+    extra = ["--noconftest", *_HOST_FILES]
+    for d in _NEEDS_GPU:
+        extra += ["--deselect", d]
+    proc, outcomes = run_suite(tmp_path, extra)
+    failed = sorted(k for k, v in outcomes.items() if v == "failed")
+    assert len(outcomes) >= 80 and not failed, (failed, proc.stdout[-3000:])
