@@ -633,7 +633,8 @@ class DistTransport:
                 for req in self.dist.batch_isend_irecv(ops):
                     req.wait()
             return [(cats, vals)]
-        parts, ops = [(cats, vals)], []
+        parts = [(self._wire(cats), self._wire(vals) if values else None)]
+        ops = []
         for w in range(1, self.workers):
             c = self._empty(counts[w], torch.int64)
             v = self._empty((counts[w], n), torch.float32) if values else None

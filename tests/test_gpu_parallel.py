@@ -127,6 +127,9 @@ def _dist_worker_shard_only(rank, world, port, q):
         q.put((rank, res.categories.tolist(),
                [(o.active_before, o.active_after) for o in res.per_layer],
                np.asarray(res.final.data).view(np.uint32).tobytes(), res.edges_processed))
+    except Exception:  # reported to the parent instead of a queue timeout
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc(), None, None, None))
     finally:
         dist.destroy_process_group()
 
@@ -145,6 +148,9 @@ def test_shard_only_two_ranks_chunk_built(cuda_ok):
     res = sorted(q.get(timeout=300) for _ in range(2))
     for p in procs:
         p.join(timeout=60)
+    errors = [r[1] for r in res if isinstance(r[1], str)]
+    assert not errors, errors[0]
+    for p in procs:
         assert p.exitcode == 0
     model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
         neurons=1024, layers=40, connections_per_neuron=32, bias_value=-0.3, seed=21))
@@ -177,6 +183,9 @@ def _dist_worker(rank, world, port, q):
         q.put((rank, res.categories.tolist(),
                [(o.active_before, o.active_after) for o in res.per_layer],
                float(np.asarray(res.final.data, np.float64).sum()), comm.total_moved))
+    except Exception:  # reported to the parent instead of a queue timeout
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc(), None, None, None))
     finally:
         dist.destroy_process_group()
 
@@ -197,6 +206,9 @@ def test_distributed_transport_two_ranks(cuda_ok):
     res = sorted(q.get(timeout=300) for _ in range(2))
     for p in procs:
         p.join(timeout=60)
+    errors = [r[1] for r in res if isinstance(r[1], str)]
+    assert not errors, errors[0]
+    for p in procs:
         assert p.exitcode == 0
     model, inputs = _edge(m=500)
     data = np.asarray(inputs.data).copy()
