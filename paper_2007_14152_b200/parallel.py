@@ -851,9 +851,12 @@ def run_batch_parallel_device(net, inputs: FeatureBatch, config: InferenceConfig
         sh.load(x, engine.host_tensor(np.ascontiguousarray(inputs.categories[cols])))
         shards[r] = sh
     torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
+    ev0.record()
     totals, comm, balance, parts = run_layers_parallel(
         net.num_layers, shards, transport, config.rebalance_threshold, w, values=values)
+    ev1.record()
     torch.cuda.synchronize()
     elapsed = time.perf_counter() - t0
     cats = torch.cat([p[0] for p in parts]).cpu().numpy().astype(np.int64)
@@ -877,5 +880,6 @@ def run_batch_parallel_device(net, inputs: FeatureBatch, config: InferenceConfig
             feature_element_reads=net.num_fp[l] * before))
     epi = edges_per_input if edges_per_input is not None else int(sum(net.nnz))
     result = engine.InferenceResult(final=final, categories=cats.copy(), per_layer=per_layer,
-                                    elapsed_seconds=elapsed, edges_processed=total * epi)
+                                    elapsed_seconds=elapsed, edges_processed=total * epi,
+                                    device_seconds=ev0.elapsed_time(ev1) / 1e3)
     return result, comm, balance

@@ -6,7 +6,7 @@ set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 for tool in memcheck racecheck synccheck; do
-  timeout 1500 compute-sanitizer --tool "$tool" --kernel-name regex:layer_kernel \
+  timeout 1500 compute-sanitizer --tool "$tool" --kernel-name kns=layer_kernel \
       --print-limit 200 --error-exitcode 9 \
       python tools/sanitize_run.py > "gpurun_out/sanitize_${tool}.log" 2>&1
   echo "$tool rc=$?" | tee -a gpurun_out/sanitize_summary.txt
