@@ -233,6 +233,7 @@ struct LayerArgs {
   const float *y_in;
   float *y_out;
   int64_t ld;
+  uint32_t ld_bytes;   // 4 * ld (< 2^32): one output row of the feature buffer
   const int32_t *a_in;
   const int64_t *cat_in;
   const int32_t *m_in;
@@ -471,6 +472,24 @@ __device__ __forceinline__ void accumulate_mask(u64 *acc, const uint32_t *recs, 
 #pragma unroll
     for (int j = 0; j < 4; j++) mask_record<R, FMA, FPL>(acc, wd[j], y[j], w, negz2);
   }
+  // the last 1-3 records of the run (cnt is exact; the run is stored padded
+  // to a whole 16-byte quad with zero words, which are not executed): two
+  // warp-uniform branches instead of 14 predicated-off FFMA2 per padding word
+  const int rem = cnt & 3;
+  if (rem) {
+    const uint4 q = *rp;
+    YVec<FPL> y;
+    y.load_s(ybase + (q.x >> (15 + Geo<FPL>::kOffShift)));
+    mask_record<R, FMA, FPL>(acc, q.x, y, w, negz2);
+    if (rem > 1) {
+      y.load_s(ybase + (q.y >> (15 + Geo<FPL>::kOffShift)));
+      mask_record<R, FMA, FPL>(acc, q.y, y, w, negz2);
+    }
+    if (rem > 2) {
+      y.load_s(ybase + (q.z >> (15 + Geo<FPL>::kOffShift)));
+      mask_record<R, FMA, FPL>(acc, q.z, y, w, negz2);
+    }
+  }
 }
 
 // NaN-propagating max / min (max.NaN.f32): the reference's comparison clamp
@@ -507,7 +526,10 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
                                                 const float *bias, int j0, int valid,
                                                 bool &tiny) {
   constexpr int H = FPL / 2;
-  const char *obase = reinterpret_cast<const char *>(A.y_out) + 4ull * (uint32_t)j0;
+  // row k's output address is one wide multiply-add off this base (the FMA
+  // pipe is the kernel's bottleneck: no per-row re-derivation of ld * 4)
+  const uint64_t obase = reinterpret_cast<uint64_t>(A.y_out) + 4ull * (uint32_t)j0;
+  const uint32_t ldb = A.ld_bytes;
   // FMA form (finite values guaranteed, else the run is redone): per feature the
   // running unsigned min of bits(v) - 1 gives both tests: v > 0 exists <=> the
   // min is not 0xffffffff, and a v in (0, tiny) exists <=> min < bits(tiny) - 1.
@@ -547,12 +569,18 @@ __device__ __forceinline__ uint32_t finish_rows(const LayerArgs &A, u64 *acc, co
 #ifdef SPDNN_ABLATE_STORE
     if (rows[k] >= 0) continue;  // diagnostics: no output stores
 #endif
-    // one IMAD.WIDE.U32 per row: row * (ld * 4) + (y_out + 4 * j0); ld * 4 < 2^32
-    float *dst = (float *)(
-        obase + (unsigned long long)(uint32_t)rows[k] * (uint32_t)(A.ld * 4));
+    // one IMAD.WIDE.U32 per row: row * (ld * 4) + (y_out + 4 * j0)
+    uint64_t da;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(da) : "r"((uint32_t)rows[k]), "r"(ldb), "l"(obase));
+    float *dst = reinterpret_cast<float *>(da);
     if (FULL) {
-      if (FPL == 4) *reinterpret_cast<float4 *>(dst) = make_float4(x[0], x[1], x[2], x[3]);
-      else *reinterpret_cast<float2 *>(dst) = make_float2(x[0], x[1]);
+      if (FPL == 4)
+        asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(da), "f"(x[0]), "f"(x[1]),
+                     "f"(x[2]), "f"(x[3])
+                     : "memory");
+      else
+        asm volatile("st.global.v2.f32 [%0], {%1, %2};" ::"l"(da), "f"(x[0]), "f"(x[1])
+                     : "memory");
     } else {
 #pragma unroll
       for (int q = 0; q < FPL; q++)
@@ -1399,6 +1427,7 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   A.y_in = y_in;
   A.y_out = y_out;
   A.ld = ld;
+  A.ld_bytes = (uint32_t)(ld * 4);
   A.a_in = a_in;
   A.cat_in = cat_in;
   A.m_in = m_in;

@@ -283,11 +283,12 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
         }
         cnt++;
       }
-      // mask records: each group's run padded to a multiple of 4 (the kernel
-      // reads 4 records per 16-byte load); the padding words are mask 0, so
-      // their FFMA2s are all predicated off (measured cheaper than a tail
-      // loop over the exact count)
+      // mask records: each group's run is stored padded to a multiple of 4
+      // words (the kernel reads 4 records per 16-byte load, so every run
+      // starts 16-byte aligned); the padding words are mask 0 and the
+      // segment keeps the exact count, so the kernel skips them
       real += cnt;
+      const int64_t exact = cnt;
       if (pl->uniform)
         while (cnt % 4) {
           pl->records.push_back(0u);
@@ -295,7 +296,7 @@ void emit(spdnn_plan *pl, const int64_t *rp, const int32_t *ci, const float *va,
         }
       if (gseg) {
         gseg->push_back((int32_t)start);
-        gseg->push_back((int32_t)cnt);
+        gseg->push_back((int32_t)exact);
       }
     }
     const int64_t rec_cnt = (int64_t)pl->records.size() / RW - rec_off;
