@@ -164,19 +164,25 @@ def measured_peaks():
 
 
 def ncu_traffic(cfg_key: str):
-    """DRAM bytes per launch of the layer kernel from the committed ncu capture
-    (profiles/*_ncu_layer*_<cfg>.json, one steady-state launch)."""
+    """DRAM bytes of one steady-state launch of the layer kernel from the
+    newest committed ncu capture (profiles/r<N>_ncu_layer<L>_<cfg>.json).
+    Returns (bytes, file name, layer index) or (None, None, None)."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*_ncu_layer*_{cfg_key}.json")))
+    import re
+    scale = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12}
+    files = glob.glob(os.path.join(ROOT, "profiles", f"r*_ncu_layer*_{cfg_key}.json"))
     if not files:
-        return None, None
+        return None, None, None
+    files.sort(key=lambda f: int(re.search(r"r(\d+)_", os.path.basename(f)).group(1)))
     with open(files[-1]) as f:
         d = json.load(f)
     try:
-        mb = float(d["dram__bytes_read.sum"][0]) + float(d["dram__bytes_write.sum"][0])
+        tot = sum(float(d[k][0]) * scale[d[k][1].lower()]
+                  for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     except (KeyError, TypeError, ValueError):
-        return None, None
-    return mb * 1e6, os.path.basename(files[-1])
+        return None, None, None
+    layer = int(re.search(r"_ncu_layer(\d+)_", os.path.basename(files[-1])).group(1))
+    return tot, os.path.basename(files[-1]), layer
 
 
 def cpu_baseline(model, inputs, sample_cols: int, threads: int, target_s: float = 0.0):
@@ -736,7 +742,7 @@ def run_ours(args, cfg):
     achieved = float(bytes_l[active].sum() / (layer_ms.mean(axis=0)[active].sum() / 1e3) / 1e9)
     peak, peak_src = measured_peaks()
     kernel_share = float(layer_ms.mean(axis=0).sum() / (ms_total / args.steps))
-    traffic, traffic_src = ncu_traffic(args.config)
+    traffic, traffic_src, traffic_layer = ncu_traffic(args.config)
     del x_dev
     torch.cuda.empty_cache()
 
@@ -780,8 +786,11 @@ def run_ours(args, cfg):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": (f"profiles/{traffic_src}: dram read+write of one "
-                                        "steady-state launch (ncu --set full)")
-                                       if traffic else None,
+                                        f"steady-state launch (layer {traffic_layer}, ncu "
+                                        "--set full); that launch's algorithmic bytes: "
+                                        f"{float(bytes_l[traffic_layer]):.4g}")
+                                       if traffic and traffic_layer is not None
+                                       and traffic_layer < L else None,
                      "peak_source": peak_src,
                      "kernel": "layer_kernel (csrc/layer.cu)",
                      "bytes_per_launch": "8*N*M_l + 6*nnz_l + 4*N",

@@ -1,6 +1,6 @@
 """Turn raw ncu outputs into the committed profile summaries.
 
-    python tools/summarize_profiles.py <tag> <ncu-rep of one layer launch> <launch-list csv> <cfg>
+    python tools/summarize_profiles.py <tag> <ncu-rep of one layer launch> <launch-list csv|-> <cfg> [layer]
 
 Writes profiles/<tag>_ncu_layer200_<cfg>.json (selected metrics of the
 `ncu --set full` capture, per launch) and profiles/<tag>_launches_<cfg>_summary.csv
@@ -33,6 +33,7 @@ METRICS = [
 
 def main():
     tag, rep, launches, cfg = sys.argv[1:5]
+    layer = sys.argv[5] if len(sys.argv) > 5 else "200"
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -44,8 +45,12 @@ def main():
         if h.startswith("smsp__average_warps_issue_stalled_") and
         h.endswith("_per_issue_active.ratio")}
     out["stall_per_issued_instruction"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:10])
-    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_layer200_{cfg}.json"), "w") as f:
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_layer{layer}_{cfg}.json"), "w") as f:
         json.dump(out, f, indent=1)
+    if launches == "-":
+        print(json.dumps({k: out[k] for k in ("gpu__time_duration.sum", "dram__bytes_read.sum",
+                                              "dram__bytes_write.sum")}))
+        return
     tot, cnt, layer_us = defaultdict(float), defaultdict(int), []
     with open(launches) as f:
         lines = [ln for ln in f if ln.startswith('"')]
