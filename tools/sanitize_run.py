@@ -39,7 +39,7 @@ def structured():
         base = (np.arange(n) * off) % n
         cols = ((base[:, None] + np.arange(k)[None, :]) % n).reshape(-1)
         vals = rng.uniform(0.02, 0.2, n * k).astype(np.float32)
-        vals *= rng.choice([-1.0, 1.0], n * k).astype(np.float32)
+        vals *= rng.choice([-1.0, 1.0], n * k, p=[0.3, 0.7]).astype(np.float32)
         layers.append(make_layer_csr(n, rows, cols, vals))
     model = NetworkModel(n, tuple(layers), np.full(n, -0.05, np.float32))
     inputs = ingest.generate_synthetic_inputs(n, 300, 0.3, seed=3)
