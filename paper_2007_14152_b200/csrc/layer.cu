@@ -42,6 +42,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -152,11 +153,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
-// cp.async.mbarrier.arrive (counted): +1 pending now, -1 when this thread's
-// earlier cp.async copies have landed
-__device__ __forceinline__ void mbar_cp_async_arrive_inc(uint32_t bar) {
-  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
-}
 // Division by a runtime divisor d >= 1 for n < 2^31 (the producer splits every
 // claimed item into tile and block, and ring counters into slot and phase):
 // one multiply-high and two shifts instead of the ~20-instruction sequence.
@@ -253,8 +249,9 @@ struct LayerArgs {
   int nbuf;            // ring depth
   uint32_t mring_off;  // producer metadata ring (after the nbuf buffers)
   uint32_t mentry_bytes;
-  int simple_wait;     // 1: consumer warps visit every (C/gpi)-th entry and (C/gpi) | nbuf
   int gpi;             // consumer work units (row groups) per item = max groups per block
+  int teams;           // > 1: the consumer warps form `teams` teams, team T takes the
+                       // entries k = T mod teams (all their units); teams | nbuf
   uint32_t act_off;    // activity bytes: [nbuf][gpi][32 lanes], one byte per lane and unit
 };
 
@@ -711,8 +708,8 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     s_wmask = __uint_as_float(A.L.weight_bits);
     for (int i = 0; i < nbuf; i++) {
       mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
-      mbar_init(empty0 + 8 * i, gpi);  // one arrival per work unit (row group) of the item
-      mbar_init(free0 + 8 * i, 1);     // the publisher's release of the slot
+      mbar_init(empty0 + 8 * i, gpi * 32);  // every lane of every work unit (row group)
+      mbar_init(free0 + 8 * i, 32);         // every publisher lane: the slot is released
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -965,9 +962,14 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
             for (int q = 0; q < FPL; q++) cp_async4(dst + 128 * q, row + max(src[q], 0), src[q] >= 0);
           }
         }
-        mbar_cp_async_arrive_inc(full);
+        // every producer thread waits for its own copies (and the metadata
+        // prefetches already in flight), then the named barrier orders all
+        // of them before the header's arrival (the rare path: the layer
+        // right after one in which features died)
+        cp_async_commit();
+        cp_async_wait<0>();
         PROF_MARK(7);  // [7] 4-byte cp.async gathers (tiles with gaps)
-        pbar();  // every producer's cp.async arrivals counted before the header's
+        pbar();
         if (ptid == 0) post_header();
       }
       // metadata for items k + kMetaAhead (descriptor) and k + kFpAhead
@@ -1022,7 +1024,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         const uint32_t word = __ballot_sync(0xffffffffu, (am >> q) & 1u);
         if (lane == q) wv = word;
       }
-      if (lane == 0) mbar_arrive(free0 + 8 * slot);
+      mbar_arrive(free0 + 8 * slot);  // each lane's activity reads are done
       if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * t + lane], wv);
       __syncwarp();
       int last = 0;
@@ -1072,33 +1074,38 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
 
   // ======================= consumer warps =======================
   // Work unit u = (ring entry k = u / gpi, row group g = u % gpi); warp w
-  // takes units w, w + C, ... Entries a warp waits on can be up to ceil(C/gpi)
-  // <= nbuf apart, so the slot's barrier may still be one phase behind: the
-  // header's entry number tells a stale phase from the awaited one.
+  // takes units w, w + C, ... launch_layer only admits mappings in which a
+  // warp consumed the slot's previous entry itself before it waits on the
+  // slot again, so the parity wait below always targets the current phase.
   const u64 negz2 = pack2(A.negz, A.negz);
   // the uniform weight, read from shared memory once: taken from the kernel
   // parameter, ptxas re-loads it from the constant bank before every
   // predicated FFMA2 instead of keeping it in a register
   const float w_mask = s_wmask;
   // unit u = warp + j*C  ->  (entry k, group g, ring slot, phase), advanced
-  // incrementally (no per-unit integer division)
-  int k = warp / gpi, g = warp - (warp / gpi) * gpi;
+  // incrementally (no per-unit integer division).
+  // Team mode (A.teams = T > 1): warp w is member w % (C/T) of team w / (C/T);
+  // a team takes every T-th entry and all its units, its members walking the
+  // groups with stride C/T. The teams are out of phase: one refills its
+  // slot while the other computes, instead of every warp finishing an entry,
+  // then waiting for the same refill together.
+  const int teams = A.teams;
+  const int tsz = C / teams, mem = warp % tsz;
+  int k, g;
+  if (teams > 1) {
+    k = warp / tsz;
+    g = mem;
+  } else {
+    k = warp / gpi;
+    g = warp - k * gpi;
+  }
+  if (g >= gpi) return;  // (team mode with fewer units than team members)
   int slot = k % nbuf;
   uint32_t phase = (uint32_t)(k / nbuf) & 1u;
   PROF_DECL
   for (;; ) {
     const char *buf = smem + slot * A.buf_bytes;
-    const volatile Header *vh = reinterpret_cast<const volatile Header *>(buf);
-    if (A.simple_wait) {
-      mbar_wait(full0 + 8 * slot, phase);
-    } else {
-      for (;;) {
-        mbar_wait(full0 + 8 * slot, phase);
-        if (vh->entry == k) break;
-        __nanosleep(256);  // the fill of entry k - nbuf is still in flight
-      }
-      mbar_wait(full0 + 8 * slot, phase);  // the phase of entry k itself
-    }
+    mbar_wait(full0 + 8 * slot, phase);  // (launch_layer: never a stale phase)
     const Header h = *reinterpret_cast<const Header *>(buf);
     PROF_MARK(0);  // [0] waiting for data
 #ifdef SPDNN_PROFILE
@@ -1143,18 +1150,29 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
                             reinterpret_cast<uint8_t *>(smem + A.act_off) + (slot * gpi + g) * 32);
       PROF_MARK(2);  // [2] epilogue
     }
-    // the unit's activity bytes (every lane's store, ordered before lane 0's
-    // arrival by __syncwarp and the mbarrier's release) are folded into the
-    // tile by the publisher warp once every unit has arrived
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty0 + 8 * slot);
-    g += C;
-    while (g >= gpi) {
-      g -= gpi;
-      k++;
-      if (++slot == nbuf) {
-        slot = 0;
-        phase ^= 1u;
+    // every lane arrives (release) after its activity byte store; the
+    // publisher warp folds the entry's bytes into the tile once all have
+    mbar_arrive(empty0 + 8 * slot);
+    if (teams > 1) {
+      g += tsz;
+      if (g >= gpi) {
+        g = mem;
+        k += teams;
+        slot += teams;
+        if (slot >= nbuf) {
+          slot -= nbuf;
+          phase ^= 1u;
+        }
+      }
+    } else {
+      g += C;
+      while (g >= gpi) {
+        g -= gpi;
+        k++;
+        if (++slot == nbuf) {
+          slot = 0;
+          phase ^= 1u;
+        }
       }
     }
     PROF_MARK(3);  // [3] unit bookkeeping, tile publishing
@@ -1240,11 +1258,43 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   const size_t budget = optin - 2048 - mring;  // static shared memory + reserve
   // + the per-unit activity bytes of each entry (gpi <= max(groups, C))
   const size_t act_unit = 32, act_max = (size_t)std::max(L.max_groups_per_block, G::kC) * act_unit;
-  const int nbuf = (int)std::min<size_t>(kMaxBufs, budget / (buf + act_max));
-  if (nbuf < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
-  // units per item: at least the block's groups, and enough that a consumer
-  // warp's consecutive units are at most nbuf ring entries apart
-  const int gpi = std::max(std::max(1, L.max_groups_per_block), (G::kC + nbuf - 1) / nbuf);
+  const int nbmax = (int)std::min<size_t>(kMaxBufs, budget / (buf + act_max));
+  if (nbmax < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
+  // Ring depth, units per entry (gpi) and consumer mapping. Every admitted
+  // mapping has each consumer warp consume the slot's previous entry itself
+  // before it waits on the slot again, so a parity wait can never see a stale
+  // phase:
+  //   team mode (T | nbuf, T | C, every member has a unit): team w/(C/T)
+  //     takes every T-th entry -- the default when the ring depth is even;
+  //   gpi >= C: each warp visits every entry;
+  //   gpi | C with (C/gpi) | nbuf: each warp visits every (C/gpi)-th entry.
+  // Among those, the most units with work per warp slot, then the deepest ring.
+  static const int teams_env = [] {
+    const char *s = std::getenv("SPDNN_TEAMS");
+    return s ? std::atoi(s) : 1;
+  }();
+  const int C = G::kC, mg = std::max(1, L.max_groups_per_block);
+  int nbuf = 0, gpi = 0, teams = 1;
+  double best = -1.0;
+  for (int nb = nbmax; nb >= 2; nb--) {
+    auto consider = [&](int gp, int tm, double util) {
+      if (util > best + 1e-9) {
+        best = util;
+        nbuf = nb;
+        gpi = gp;
+        teams = tm;
+      }
+    };
+    const int T = teams_env;
+    if (T > 1 && nb % T == 0 && C % T == 0 && mg >= C / T) {
+      const int tsz = C / T;
+      consider(mg, T, (double)mg / (double)(((mg + tsz - 1) / tsz) * tsz));
+    }
+    if (mg >= C) consider(mg, 1, 1.0);
+    for (int d = mg; d < C; d++)
+      if (C % d == 0 && nb % (C / d) == 0) consider(d, 1, (double)mg / d);
+    if (mg < C) consider(C, 1, (double)mg / C);
+  }
   const size_t smem = (size_t)nbuf * buf + mring + (size_t)nbuf * gpi * act_unit;
   A.mring_off = (uint32_t)(nbuf * buf);
   A.act_off = (uint32_t)(nbuf * buf + mring);
@@ -1254,9 +1304,7 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   A.buf_bytes = (uint32_t)buf;
   A.nbuf = nbuf;
   A.gpi = gpi;
-  // warp w visits entries w/gpi + j*(C/gpi): when that stride divides nbuf the
-  // warp consumed entry k - nbuf itself before waiting on k (no stale phase)
-  A.simple_wait = (G::kC % gpi == 0 && nbuf % (G::kC / gpi) == 0) ? 1 : 0;
+  A.teams = teams;
   // the smem attribute and the occupancy query cost several microseconds of
   // host time each; a layer loop launches every ~30 us at small batches, so
   // both are cached per (device, kernel): the attribute only ever grows
