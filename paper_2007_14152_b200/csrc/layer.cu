@@ -42,7 +42,6 @@
 #include <stdint.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -250,8 +249,6 @@ struct LayerArgs {
   uint32_t mring_off;  // producer metadata ring (after the nbuf buffers)
   uint32_t mentry_bytes;
   int gpi;             // consumer work units (row groups) per item = max groups per block
-  int teams;           // > 1: the consumer warps form `teams` teams, team T takes the
-                       // entries k = T mod teams (all their units); teams | nbuf
   uint32_t act_off;    // activity bytes: [nbuf][gpi][32 lanes], one byte per lane and unit
 };
 
@@ -674,6 +671,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     layer_kernel(const __grid_constant__ LayerArgs A) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) u64 s_full[kMaxBufs], s_empty[kMaxBufs], s_free[kMaxBufs];
+  __shared__ __align__(8) u64 s_rfree[kMaxBufs];
   __shared__ float s_wmask;
 #ifdef SPDNN_PROFILE
   __shared__ long long s_tgr[kMaxBufs], s_tpost[kMaxBufs], s_tempty[kMaxBufs];
@@ -703,13 +701,15 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   const uint32_t full0 = (uint32_t)__cvta_generic_to_shared(&s_full[0]);
   const uint32_t empty0 = (uint32_t)__cvta_generic_to_shared(&s_empty[0]);
   const uint32_t free0 = (uint32_t)__cvta_generic_to_shared(&s_free[0]);
+  const uint32_t rfree0 = (uint32_t)__cvta_generic_to_shared(&s_rfree[0]);
 
   if (tid == 0) {
     s_wmask = __uint_as_float(A.L.weight_bits);
     for (int i = 0; i < nbuf; i++) {
       mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
       mbar_init(empty0 + 8 * i, gpi * 32);  // every lane of every work unit (row group)
-      mbar_init(free0 + 8 * i, 32);         // every publisher lane: the slot is released
+      mbar_init(free0 + 8 * i, 32);         // every publisher lane: activity bytes read
+      mbar_init(rfree0 + 8 * i, gpi * 32);  // every unit's lanes: staged rows read
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -878,7 +878,14 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const uint32_t kq = fnbuf.div((uint32_t)k);
       const int slot = k - (int)kq * nbuf;
       const uint32_t phase = kq & 1u;
-      if (pw == 0) mbar_wait(free0 + 8 * slot, phase ^ 1u);  // others park at the bar.sync below
+      // Refill of ring slot `slot` (entry k; the slot last held entry k - nbuf),
+      // in three steps that each wait only for what they overwrite:
+      //   1. the staged rows, once every unit of k - nbuf is past its record
+      //      loop (rows_free) -- the epilogues still run;
+      //   2. block metadata and records, once every unit is done (empty);
+      //   3. the header arrival, once the publisher has read the units'
+      //      activity bytes (free), which entry k's units overwrite.
+      if (pw == 0) mbar_wait(rfree0 + 8 * slot, phase ^ 1u);  // others park at the bar.sync below
 #ifdef SPDNN_PROFILE
       if (ptid == 0) {
         const long long now = clock64();
@@ -890,7 +897,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         s_tfirst[slot] = ~0ull;
       }
 #endif
-      PROF_MARK(0);  // [0] waiting for an empty slot
+      PROF_MARK(0);  // [0] waiting for the slot's rows
       const uint32_t full = full0 + 8 * slot;
       const uint32_t buf = sbase + slot * A.buf_bytes;
       const uint32_t smeta = buf + kHeaderBytes;
@@ -899,21 +906,61 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const int meta_words = ((fp_cnt + 3) & ~3) + ((2 * ng + 2 * R * ng + 3) & ~3);
       const uint32_t rec_b = (uint32_t)((rec_cnt * RW * 4 + 15) & ~15);
       const int quads = (fp_cnt + 3) >> 2;
-      if (ptid == 0) {
 #ifdef SPDNN_ABLATE_STAGE
-        const uint32_t tx = (uint32_t)meta_words * 4u + rec_b;
+      const bool gather = false;  // diagnostics: staged rows are not copied
 #else
-        const uint32_t tx = (uint32_t)meta_words * 4u + rec_b +
-                            (contig ? (uint32_t)quads * 4u * G::kRow : 0u);
+      const bool gather = contig;
 #endif
-        mbar_expect_tx(full, tx);
+      if (ptid == 0)  // the phase cannot complete before the header's arrival
+        mbar_expect_tx(full, (uint32_t)meta_words * 4u + rec_b +
+                                 (gather ? (uint32_t)quads * 4u * G::kRow : 0u));
+      pbar();  // the rows may be overwritten; expected bytes registered
+      PROF_MARK(1);  // [1] barrier A
+      if (gather) {
+        if (qd0 < quads)
+          tma_gather4(sy + (uint32_t)qd0 * 4u * G::kRow, &A.tmap_in, p0, c4.x, c4.y, c4.z, c4.w,
+                      full);
+        for (int qd = P * 32 + ptid; qd < quads; qd += P * 32) {  // footprints > 512 rows
+          int4 c = *reinterpret_cast<const int4 *>(sfp + 4 * qd);
+          if (4 * qd + 1 >= fp_cnt) c.y = c.x;
+          if (4 * qd + 2 >= fp_cnt) c.z = c.x;
+          if (4 * qd + 3 >= fp_cnt) c.w = c.x;
+          tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c.x, c.y, c.z, c.w, full);
+        }
+        PROF_MARK(6);  // [6] TMA gather4 issue (contiguous tiles)
+      } else if (!contig) {
+        // staged rows s = 32 pw .. : the warp's 32 lanes copy the row's T
+        // features with 4-byte cp.async (tiles whose columns have gaps: the
+        // layer right after one in which features died); every producer
+        // thread waits for its own copies (and the metadata prefetches in
+        // flight), the named barrier below orders all of them before the
+        // header's arrival
+        for (int s0 = pw * 32; s0 < fp_cnt; s0 += P * 32) {
+          const int my = s0 + lane < fp_cnt ? sfp[s0 + lane] : 0;
+          const int cnt = min(32, fp_cnt - s0);
+          for (int i = 0; i < cnt; i++) {
+            const int64_t c = __shfl_sync(0xffffffffu, my, i);
+            const float *row = A.y_in + c * A.ld;
+            const uint32_t dst = sy + (uint32_t)(s0 + i) * G::kRow + 4 * lane;
+#pragma unroll
+            for (int q = 0; q < FPL; q++) cp_async4(dst + 128 * q, row + max(src[q], 0), src[q] >= 0);
+          }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        PROF_MARK(7);  // [7] 4-byte cp.async gathers (tiles with gaps)
       }
-      pbar();  // expected bytes registered before any copy can complete
-      PROF_MARK(1);  // [1] barrier A (slot free, expected bytes set)
-      if (ptid == 0 && meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
-      if (ptid == 32 && rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
-      PROF_MARK(2);  // [2] bulk copies of meta + records
-      auto post_header = [&]() {
+      if (pw == 0) {
+        mbar_wait(empty0 + 8 * slot, phase ^ 1u);  // every unit of k - nbuf is done
+        if (lane == 0) {
+          if (meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
+          if (rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
+        }
+        PROF_MARK(2);  // [2] bulk copies of meta + records
+        mbar_wait(free0 + 8 * slot, phase ^ 1u);  // activity bytes of k - nbuf read
+      }
+      if (!contig) pbar();  // every producer's cp.async copies landed
+      if (ptid == 0) {
         Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
         h->item = item;
         h->entry = k;
@@ -927,50 +974,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         s_tpost[slot] = clock64();
 #endif
         mbar_arrive(full);
-      };
-#ifdef SPDNN_ABLATE_STAGE
-      if (contig) {  // diagnostics: staged rows are not copied (not expected either)
-        if (ptid == 0) post_header();
-      } else
-#endif
-      if (contig) {
-        if (qd0 < quads)
-          tma_gather4(sy + (uint32_t)qd0 * 4u * G::kRow, &A.tmap_in, p0, c4.x, c4.y, c4.z, c4.w,
-                      full);
-        for (int qd = P * 32 + ptid; qd < quads; qd += P * 32) {  // footprints > 512 rows
-          int4 c = *reinterpret_cast<const int4 *>(sfp + 4 * qd);
-          if (4 * qd + 1 >= fp_cnt) c.y = c.x;
-          if (4 * qd + 2 >= fp_cnt) c.z = c.x;
-          if (4 * qd + 3 >= fp_cnt) c.w = c.x;
-          tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c.x, c.y, c.z, c.w, full);
-        }
-        PROF_MARK(6);  // [6] TMA gather4 issue (contiguous tiles)
-        // every byte of the fill was expected up front, so the arrival can go
-        // before the other producers finish issuing: the phase completes only
-        // once all of them have landed
-        if (ptid == 0) post_header();
-      } else {
-        // staged rows s = 32 pw .. : the warp's 32 lanes copy the row's T features
-        for (int s0 = pw * 32; s0 < fp_cnt; s0 += P * 32) {
-          const int my = s0 + lane < fp_cnt ? sfp[s0 + lane] : 0;
-          const int cnt = min(32, fp_cnt - s0);
-          for (int i = 0; i < cnt; i++) {
-            const int64_t c = __shfl_sync(0xffffffffu, my, i);
-            const float *row = A.y_in + c * A.ld;
-            const uint32_t dst = sy + (uint32_t)(s0 + i) * G::kRow + 4 * lane;
-#pragma unroll
-            for (int q = 0; q < FPL; q++) cp_async4(dst + 128 * q, row + max(src[q], 0), src[q] >= 0);
-          }
-        }
-        // every producer thread waits for its own copies (and the metadata
-        // prefetches already in flight), then the named barrier orders all
-        // of them before the header's arrival (the rare path: the layer
-        // right after one in which features died)
-        cp_async_commit();
-        cp_async_wait<0>();
-        PROF_MARK(7);  // [7] 4-byte cp.async gathers (tiles with gaps)
-        pbar();
-        if (ptid == 0) post_header();
       }
       // metadata for items k + kMetaAhead (descriptor) and k + kFpAhead
       // (staged rows; its descriptor landed with this iteration's wait):
@@ -985,14 +988,61 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     return;
   }
 
+  // the global part of a finished item (tile t, this lane's activity word
+  // wv): OR it into the tile's words, count the tile's finished blocks, and
+  // the item that completes tile t appends the tile's survivors to a_out /
+  // cat_out (pruning without a pass over Y)
+  auto account = [&](const int t, uint32_t wv) {
+    if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * t + lane], wv);
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      // release our activity bits before the count; the last arrival
+      // acquires everyone's (acq_rel instead of a full __threadfence)
+      int old;
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n"
+                   : "=r"(old)
+                   : "l"(A.tile_done + t)
+                   : "memory");
+      last = old == nb - 1;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      if (lane < FPL) {
+        wv = atomicOr(&A.tile_alive[FPL * t + lane], 0u);
+        A.tile_alive[FPL * t + lane] = 0u;
+      }
+      if (lane == 0) A.tile_done[t] = 0;
+      uint32_t mw[FPL];
+      int tot = 0, below = 0;
+#pragma unroll
+      for (int q = 0; q < FPL; q++) {
+        mw[q] = __shfl_sync(0xffffffffu, wv, q);
+        tot += __popc(mw[q]);
+        below += __popc(mw[q] & ((1u << lane) - 1u));  // alive features of lanes < this
+      }
+      int base = 0;
+      if (lane == 0 && tot) base = atomicAdd(A.m_out, tot);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      // this lane's features FPL*lane + q, in feature order
+      int rank = base + below;
+#pragma unroll
+      for (int q = 0; q < FPL; q++) {
+        if ((mw[q] >> lane) & 1u) {
+          const int j = t * T + FPL * lane + q;
+          A.a_out[rank] = j;
+          A.cat_out[rank] = A.cat_in[j];
+          rank++;
+        }
+      }
+    }
+  };
+
   if (warp == C + P) {
     // ======================= publisher warp =======================
-    // Once every unit of ring entry k has arrived on empty[slot], read and
-    // clear the entry's activity bits, release the slot to the producer
-    // (free[slot]) and only then do the global part off the fill path: OR
-    // the bits into the tile's word, count the tile's finished blocks, and
-    // the item that completes tile t appends the tile's survivors to
-    // a_out / cat_out (pruning without a pass over Y).
+    // Once every unit of ring entry k has arrived on empty[slot]: OR the
+    // units' activity bytes into the tile's words, release the slot to the
+    // producer (free[slot]), then account() for the item off the fill path.
     for (int k = 0;; k++) {
       const int slot = k % nbuf;
       const uint32_t phase = (uint32_t)(k / nbuf) & 1u;
@@ -1025,49 +1075,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         if (lane == q) wv = word;
       }
       mbar_arrive(free0 + 8 * slot);  // each lane's activity reads are done
-      if (lane < FPL && wv) atomicOr(&A.tile_alive[FPL * t + lane], wv);
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) {
-        // release our activity bits before the count; the last arrival
-        // acquires everyone's (acq_rel instead of a full __threadfence)
-        int old;
-        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;\n"
-                     : "=r"(old)
-                     : "l"(A.tile_done + t)
-                     : "memory");
-        last = old == nb - 1;
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (last) {
-        if (lane < FPL) {
-          wv = atomicOr(&A.tile_alive[FPL * t + lane], 0u);
-          A.tile_alive[FPL * t + lane] = 0u;
-        }
-        if (lane == 0) A.tile_done[t] = 0;
-        uint32_t mw[FPL];
-        int tot = 0, below = 0;
-#pragma unroll
-        for (int q = 0; q < FPL; q++) {
-          mw[q] = __shfl_sync(0xffffffffu, wv, q);
-          tot += __popc(mw[q]);
-          below += __popc(mw[q] & ((1u << lane) - 1u));  // alive features of lanes < this
-        }
-        int base = 0;
-        if (lane == 0 && tot) base = atomicAdd(A.m_out, tot);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        // this lane's features FPL*lane + q, in feature order
-        int rank = base + below;
-#pragma unroll
-        for (int q = 0; q < FPL; q++) {
-          if ((mw[q] >> lane) & 1u) {
-            const int j = t * T + FPL * lane + q;
-            A.a_out[rank] = j;
-            A.cat_out[rank] = A.cat_in[j];
-            rank++;
-          }
-        }
-      }
+      account(t, wv);
     }
     return;
   }
@@ -1084,22 +1092,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   const float w_mask = s_wmask;
   // unit u = warp + j*C  ->  (entry k, group g, ring slot, phase), advanced
   // incrementally (no per-unit integer division).
-  // Team mode (A.teams = T > 1): warp w is member w % (C/T) of team w / (C/T);
-  // a team takes every T-th entry and all its units, its members walking the
-  // groups with stride C/T. The teams are out of phase: one refills its
-  // slot while the other computes, instead of every warp finishing an entry,
-  // then waiting for the same refill together.
-  const int teams = A.teams;
-  const int tsz = C / teams, mem = warp % tsz;
-  int k, g;
-  if (teams > 1) {
-    k = warp / tsz;
-    g = mem;
-  } else {
-    k = warp / gpi;
-    g = warp - k * gpi;
-  }
-  if (g >= gpi) return;  // (team mode with fewer units than team members)
+  int k = warp / gpi, g = warp - (warp / gpi) * gpi;
   int slot = k % nbuf;
   uint32_t phase = (uint32_t)(k / nbuf) & 1u;
   PROF_DECL
@@ -1133,6 +1126,9 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
                                    meta[seg_base + 2 * g + 1], ybase, negz2);
       }
       if (h.nst > 1) accumulate_global<R, FMA, FPL, MASK>(A, acc, h.b, h.t, lane, M, negz2);
+      // this lane is done with the staged rows: the producer may refill them
+      // while the epilogue runs
+      mbar_arrive(rfree0 + 8 * slot);
       PROF_MARK(1);  // [1] record loop
       // output rows and their biases (staged with the block metadata) are read
       // only now, so they hold no registers across the record loop
@@ -1149,30 +1145,19 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       epilogue<R, FMA, FPL>(A, acc, rows, bias, h.t, lane, M,
                             reinterpret_cast<uint8_t *>(smem + A.act_off) + (slot * gpi + g) * 32);
       PROF_MARK(2);  // [2] epilogue
+    } else {
+      mbar_arrive(rfree0 + 8 * slot);  // (a unit past the block's groups)
     }
     // every lane arrives (release) after its activity byte store; the
     // publisher warp folds the entry's bytes into the tile once all have
     mbar_arrive(empty0 + 8 * slot);
-    if (teams > 1) {
-      g += tsz;
-      if (g >= gpi) {
-        g = mem;
-        k += teams;
-        slot += teams;
-        if (slot >= nbuf) {
-          slot -= nbuf;
-          phase ^= 1u;
-        }
-      }
-    } else {
-      g += C;
-      while (g >= gpi) {
-        g -= gpi;
-        k++;
-        if (++slot == nbuf) {
-          slot = 0;
-          phase ^= 1u;
-        }
+    g += C;
+    while (g >= gpi) {
+      g -= gpi;
+      k++;
+      if (++slot == nbuf) {
+        slot = 0;
+        phase ^= 1u;
       }
     }
     PROF_MARK(3);  // [3] unit bookkeeping, tile publishing
@@ -1260,40 +1245,27 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   const size_t act_unit = 32, act_max = (size_t)std::max(L.max_groups_per_block, G::kC) * act_unit;
   const int nbmax = (int)std::min<size_t>(kMaxBufs, budget / (buf + act_max));
   if (nbmax < 2) return spdnn_fail(SPDNN_ERANGE, "layer: staged tile exceeds shared memory");
-  // Ring depth, units per entry (gpi) and consumer mapping. Every admitted
-  // mapping has each consumer warp consume the slot's previous entry itself
-  // before it waits on the slot again, so a parity wait can never see a stale
-  // phase:
-  //   team mode (T | nbuf, T | C, every member has a unit): team w/(C/T)
-  //     takes every T-th entry -- the default when the ring depth is even;
+  // Ring depth and units per entry (gpi). Every admitted mapping has each
+  // consumer warp consume the slot's previous entry itself before it waits
+  // on the slot again, so a parity wait can never see a stale phase:
   //   gpi >= C: each warp visits every entry;
   //   gpi | C with (C/gpi) | nbuf: each warp visits every (C/gpi)-th entry.
   // Among those, the most units with work per warp slot, then the deepest ring.
-  static const int teams_env = [] {
-    const char *s = std::getenv("SPDNN_TEAMS");
-    return s ? std::atoi(s) : 1;
-  }();
   const int C = G::kC, mg = std::max(1, L.max_groups_per_block);
-  int nbuf = 0, gpi = 0, teams = 1;
+  int nbuf = 0, gpi = 0;
   double best = -1.0;
   for (int nb = nbmax; nb >= 2; nb--) {
-    auto consider = [&](int gp, int tm, double util) {
+    auto consider = [&](int gp, double util) {
       if (util > best + 1e-9) {
         best = util;
         nbuf = nb;
         gpi = gp;
-        teams = tm;
       }
     };
-    const int T = teams_env;
-    if (T > 1 && nb % T == 0 && C % T == 0 && mg >= C / T) {
-      const int tsz = C / T;
-      consider(mg, T, (double)mg / (double)(((mg + tsz - 1) / tsz) * tsz));
-    }
-    if (mg >= C) consider(mg, 1, 1.0);
+    if (mg >= C) consider(mg, 1.0);
     for (int d = mg; d < C; d++)
-      if (C % d == 0 && nb % (C / d) == 0) consider(d, 1, (double)mg / d);
-    if (mg < C) consider(C, 1, (double)mg / C);
+      if (C % d == 0 && nb % (C / d) == 0) consider(d, (double)mg / d);
+    if (mg < C) consider(C, (double)mg / C);
   }
   const size_t smem = (size_t)nbuf * buf + mring + (size_t)nbuf * gpi * act_unit;
   A.mring_off = (uint32_t)(nbuf * buf);
@@ -1304,7 +1276,6 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   A.buf_bytes = (uint32_t)buf;
   A.nbuf = nbuf;
   A.gpi = gpi;
-  A.teams = teams;
   // the smem attribute and the occupancy query cost several microseconds of
   // host time each; a layer loop launches every ~30 us at small batches, so
   // both are cached per (device, kernel): the attribute only ever grows

@@ -88,7 +88,35 @@ __device__ __forceinline__ void accumulate_mask_pipe(u64 *acc, const uint32_t *r
   }
 }
 
-template <int UNROLL, bool PIPE = false>
+// MODE 1: every row unpredicated; 2: staged rows replaced by registers (no
+// feature LDS); 3: neither record nor feature loads (pure FFMA2 stream)
+template <int R, int MODE>
+__device__ __forceinline__ void accumulate_mode(u64 *acc, const uint32_t *recs, int cnt,
+                                                uint32_t ybase, float w) {
+  const uint4 *rp = reinterpret_cast<const uint4 *>(recs);
+  const uint4 *const end = rp + (cnt >> 2);
+  u64 yr0 = ybase, yr1 = ybase + 1;
+#pragma unroll 2
+  for (; rp < end; rp++) {
+    const uint4 q = MODE == 3 ? make_uint4(0xfeu, 0xfeu, 0xfeu, 0xfeu) : *rp;
+    const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+    YV y[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      if (MODE >= 2) {
+        y[j].v[0] = yr0 + j;
+        y[j].v[1] = yr1 ^ wd[j];
+      } else {
+        y[j].load_s(ybase + (wd[j] >> 15));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) mask_record<R>(acc, MODE == 1 ? 0xfeu : wd[j], y[j], w);
+    yr0 += 4;
+  }
+}
+
+template <int UNROLL, bool PIPE = false, int MODE = 0>
 __global__ void __launch_bounds__(1024, 1)
     loop_kernel(float *out, int reps, int cnt, const float *wp) {
   extern __shared__ __align__(128) char smem[];
@@ -117,7 +145,8 @@ __global__ void __launch_bounds__(1024, 1)
   const uint32_t *g = recs + (warp % 20) * 40;
   const uint32_t yb = full + 16 * lane;
   for (int rep = 0; rep < reps; rep++) {
-    if (PIPE) accumulate_mask_pipe<7, UNROLL>(acc, g, cnt, yb, w);
+    if (MODE) accumulate_mode<7, MODE>(acc, g, cnt, yb, w);
+    else if (PIPE) accumulate_mask_pipe<7, UNROLL>(acc, g, cnt, yb, w);
     else accumulate_mask<7, UNROLL>(acc, g, cnt, yb, w);
   }
   float s = 0;
@@ -158,6 +187,9 @@ int main() {
            name, warps, per_smsp_clk, per_smsp_clk / 0.5);
   };
   for (int warps : {4, 8, 12, 16, 20, 24, 28, 32}) run(loop_kernel<2>, "u2_sliding", warps, 40);
+  for (int warps : {8, 20}) run(loop_kernel<2, false, 1>, "mode1_unpredicated", warps, 40);
+  for (int warps : {8, 20}) run(loop_kernel<2, false, 2>, "mode2_no_feature_lds", warps, 40);
+  for (int warps : {8, 20}) run(loop_kernel<2, false, 3>, "mode3_no_lds", warps, 40);
   for (int warps : {4, 8, 12, 16, 20, 24}) run(loop_kernel<1, true>, "pipe_u1", warps, 40);
   for (int warps : {4, 8, 12, 16, 20, 24}) run(loop_kernel<2, true>, "pipe_u2", warps, 40);
   for (int warps : {4, 8, 12, 16, 20}) run(loop_kernel<2>, "u2_fullmask", warps, -40);

@@ -63,7 +63,8 @@ __device__ __forceinline__ void cp16(uint32_t s, const void *g) {
 // mode 0: gather4 (P producer warps, lane-dealt), 1: bulk per row, 2: cp.async 16 B
 template <int P>
 __global__ void __launch_bounds__((P + 1) * 32, 1)
-    stage(const __grid_constant__ CUtensorMap tm, const float *y, int ld, int nrows_src,
+    stage(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmb,
+          int br, const float *y, int ld, int nrows_src,
           int rows, int nslot, int items, int mode, unsigned long long *cycles) {
   extern __shared__ __align__(128) char smem[];
   __shared__ __align__(8) unsigned long long full[8], empty[8];
@@ -102,6 +103,21 @@ __global__ void __launch_bounds__((P + 1) * 32, 1)
             rr[j] = (r >> 4) % nrows_src;
           }
           tma_gather4(dst + qd * 4 * kRowB, &tm, col, rr[0], rr[1], rr[2], rr[3], f0 + 8 * s);
+        }
+      } else if (mode == 3) {
+        // rows consecutive tensor rows from a random start: 2-D tile boxes of
+        // br rows x 128 columns, dealt lane-major over the producer warps
+        const int nbox = (rows + br - 1) / br;
+        if (ptid == 0) mbar_expect_tx(f0 + 8 * s, nbox * br * kRowB);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(P * 32));
+        const int r0 = (int)((h >> 4) % (unsigned)(nrows_src - rows - br));
+        const int bx = lane * P + warp;
+        if (bx < nbox) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst + bx * br * kRowB),
+              "l"(reinterpret_cast<uint64_t>(&tmb)), "r"(col), "r"(r0 + bx * br), "r"(f0 + 8 * s)
+              : "memory");
         }
       } else if (mode == 1) {
         if (ptid == 0) mbar_expect_tx(f0 + 8 * s, slot_b);
@@ -148,7 +164,8 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
   auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  CUtensorMap tm;
+  CUtensorMap tm, tmb[3];
+  const int brs[3] = {8, 32, 64};
   cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)nrows_big};
   cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
   cuuint32_t box[2] = {128, 1}, es[2] = {1, 1};
@@ -158,34 +175,55 @@ int main() {
     printf("tensor map failed\n");
     return 1;
   }
-  const char *names[3] = {"gather4", "bulk/row", "cp.async16"};
-  printf("mode        rows slots srcrows   GB/s(all SMs)  B/clk/SM\n");
-  for (int mode = 0; mode < 3; mode++)
-    for (int rows : {64, 136})
-      for (int nslot : {2, 3, 4, 6})
-        for (int src : {nrows_big, 256}) {
-          const size_t sm_b = (size_t)rows * kRowB * nslot;
-          if (sm_b > 220 * 1024) continue;
-          auto fn = stage<4>;
-          CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b));
-          const int items = 400;
-          fn<<<sms, 160, sm_b>>>(tm, y, ld, src, rows, nslot, 20, mode, cyc);  // warm
-          CK(cudaDeviceSynchronize());
-          CK(cudaMemset(cyc, 0, 8));
-          cudaEvent_t a, b;
-          cudaEventCreate(&a);
-          cudaEventCreate(&b);
-          cudaEventRecord(a);
-          fn<<<sms, 160, sm_b>>>(tm, y, ld, src, rows, nslot, items, mode, cyc);
-          cudaEventRecord(b);
-          CK(cudaEventSynchronize(b));
-          float ms;
-          cudaEventElapsedTime(&ms, a, b);
-          unsigned long long c;
-          CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
-          const double bytes = (double)sms * items * rows * kRowB;
-          printf("%-10s %5d %5d %7d   %10.1f   %8.2f\n", names[mode], rows, nslot, src,
-                 bytes / ms / 1e6, (double)items * rows * kRowB / ((double)c / sms));
-        }
+  for (int i = 0; i < 3; i++) {
+    cuuint32_t bb[2] = {128, (cuuint32_t)brs[i]};
+    if (enc(&tmb[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, y, dims, strides, bb, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      printf("box tensor map failed\n");
+      return 1;
+    }
+  }
+  printf("mode        br  rows slots srcrows   GB/s(all SMs)  B/clk/SM\n");
+  struct Case { int mode, bri, rows, nslot, src; };
+  std::vector<Case> cases;
+  for (int rows : {136, 168})
+    for (int nslot : {2, 3}) {
+      cases.push_back({0, 0, rows, nslot, nrows_big});
+      for (int bi = 0; bi < 3; bi++) cases.push_back({3, bi, rows, nslot, nrows_big});
+      cases.push_back({2, 0, rows, nslot, nrows_big});
+    }
+  for (int rows : {168}) {
+    cases.push_back({0, 0, rows, 2, 256 * 4});
+    cases.push_back({3, 0, rows, 2, 256 * 4});
+  }
+  for (const Case &cs : cases) {
+    const int br = brs[cs.bri];
+    const int srows = cs.mode == 3 ? (cs.rows + br - 1) / br * br : (cs.rows + 3) / 4 * 4;
+    const size_t sm_b = (size_t)srows * kRowB * cs.nslot;
+    if (sm_b > 220 * 1024) continue;
+    auto fn = stage<4>;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_b));
+    const int items = 400;
+    // slot stride = srows rows (the kernel uses rows * kRowB as the slot size)
+    fn<<<sms, 160, sm_b>>>(tm, tmb[cs.bri], br, y, ld, cs.src, srows, cs.nslot, 20, cs.mode, cyc);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemset(cyc, 0, 8));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    fn<<<sms, 160, sm_b>>>(tm, tmb[cs.bri], br, y, ld, cs.src, srows, cs.nslot, items, cs.mode, cyc);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    unsigned long long c;
+    CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
+    const double bytes = (double)sms * items * srows * kRowB;
+    const char *nm = cs.mode == 0 ? "gather4" : (cs.mode == 3 ? "box" : "cp.async16");
+    printf("%-10s %3d %5d %5d %7d   %10.1f   %8.2f\n", nm, cs.mode == 3 ? br : 4, srows,
+           cs.nslot, cs.src, bytes / ms / 1e6, (double)items * srows * kRowB / ((double)c / sms));
+  }
   return 0;
 }
