@@ -228,6 +228,11 @@ int spdnn_gather_out(const float *y, int64_t n, int64_t ld, const int32_t *a,
  * releases). n <= 24. Diagnostics only. */
 int spdnn_profile_read(uint64_t *out, int32_t n, int32_t reset);
 
+/* Per-ring-entry clock64 timeline of CTA 0 of the last layer launches, when
+ * the library was built with -DSPDNN_TRACE (zero otherwise): out[12*k + i]
+ * for entry k < 96 (layer.cu, g_trace). n <= 1152. Diagnostics only. */
+int spdnn_trace_read(int64_t *out, int32_t n);
+
 /* Threadblocks per SM the layer kernel runs with (for diagnostics). */
 int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_sm,
                           int32_t *threads_per_cta);

@@ -114,6 +114,8 @@ def lib():
         L.spdnn_gather_out.argtypes = [P, i64, i64, P, P, i64, P, P]
         L.spdnn_profile_read.argtypes = [P, i32, i32]
         L.spdnn_profile_read.restype = ctypes.c_int
+        L.spdnn_trace_read.argtypes = [P, i32]
+        L.spdnn_trace_read.restype = ctypes.c_int
         L.spdnn_last_error.restype = ctypes.c_char_p
         L.spdnn_version.restype = ctypes.c_char_p
         for name in ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
@@ -140,5 +142,5 @@ EXPORTED = ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
             "spdnn_plan_export", "spdnn_plan_free", "spdnn_layer_forward",
             "spdnn_infer_layers", "spdnn_infer_layers_timed", "spdnn_transpose_in",
             "spdnn_gather_out",
-            "spdnn_layer_occupancy", "spdnn_profile_read", "spdnn_last_error",
+            "spdnn_layer_occupancy", "spdnn_profile_read", "spdnn_trace_read", "spdnn_last_error",
             "spdnn_version")

@@ -121,11 +121,24 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
                : "memory");
 }
 // Blocks (suspended, up to the time hint) until the phase with `parity` is done.
+#ifndef SPDNN_WAIT_TEST
+#define SPDNN_WAIT_TEST 0  // 1: spin on test_wait instead of the suspending try_wait
+#endif
 #ifndef SPDNN_WAIT_HINT_NS
 #define SPDNN_WAIT_HINT_NS 0  // 0: try_wait without a suspend-time hint
 #endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-#if SPDNN_WAIT_HINT_NS > 0
+#if SPDNN_WAIT_TEST
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+#elif SPDNN_WAIT_HINT_NS > 0
   asm volatile(
       "{\n"
       " .reg .pred p;\n"
@@ -202,6 +215,23 @@ __device__ unsigned long long g_prof[16];
 // last unit arrived), [3] release (last unit -> producer regains the slot),
 // [4] entries, [5] releases; SM-local clock64 differences summed over entries
 __device__ unsigned long long g_chain[8];
+// per-entry timeline of CTA 0 (build with -DSPDNN_TRACE; diagnostics): for
+// ring entries k < 96, clock64 at [0] rows free (grant), [1] producer warp 0
+// issued its gathers, [2] units done (empty), [3] publisher done (free),
+// [4] header posted, [5]/[6]/[7] consumer warp 0 start / loop done / unit
+// done, [8]/[9]/[10] the same for the last consumer warp, [11] publisher
+// saw empty; read with spdnn_trace_read()
+__device__ long long g_trace[96][12];
+#ifdef SPDNN_TRACE
+#define TRACE(k, i)                                                    \
+  do {                                                                 \
+    if (blockIdx.x == 0 && lane == 0 && (k) < 96) g_trace[(k)][(i)] = clock64(); \
+  } while (0)
+#else
+#define TRACE(k, i) \
+  do {              \
+  } while (0)
+#endif
 #ifdef SPDNN_PROFILE
 #define PROF_DECL                          \
   unsigned long long pf_[8] = {0};         \
@@ -897,6 +927,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         s_tfirst[slot] = ~0ull;
       }
 #endif
+      if (pw == 0) TRACE(k, 0);
       PROF_MARK(0);  // [0] waiting for the slot's rows
       const uint32_t full = full0 + 8 * slot;
       const uint32_t buf = sbase + slot * A.buf_bytes;
@@ -927,6 +958,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
           if (4 * qd + 3 >= fp_cnt) c.w = c.x;
           tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c.x, c.y, c.z, c.w, full);
         }
+        if (pw == 0) TRACE(k, 1);
         PROF_MARK(6);  // [6] TMA gather4 issue (contiguous tiles)
       } else if (!contig) {
         // staged rows s = 32 pw .. : the warp's 32 lanes copy the row's T
@@ -952,12 +984,14 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
       if (pw == 0) {
         mbar_wait(empty0 + 8 * slot, phase ^ 1u);  // every unit of k - nbuf is done
+        TRACE(k, 2);
         if (lane == 0) {
           if (meta_words) bulk_g2s(smeta, A.L.meta + meta_off, meta_words * 4, full);
           if (rec_b) bulk_g2s(srec, A.L.records + (int64_t)rec_off * RW, rec_b, full);
         }
         PROF_MARK(2);  // [2] bulk copies of meta + records
         mbar_wait(free0 + 8 * slot, phase ^ 1u);  // activity bytes of k - nbuf read
+        TRACE(k, 3);
       }
       if (!contig) pbar();  // every producer's cp.async copies landed
       if (ptid == 0) {
@@ -974,6 +1008,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         s_tpost[slot] = clock64();
 #endif
         mbar_arrive(full);
+        TRACE(k, 4);
       }
       // metadata for items k + kMetaAhead (descriptor) and k + kFpAhead
       // (staged rows; its descriptor landed with this iteration's wait):
@@ -1051,6 +1086,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       const int t = reinterpret_cast<const volatile Header *>(smem + slot * A.buf_bytes)->t;
       if (item < 0) break;
       mbar_wait(empty0 + 8 * slot, phase);
+      TRACE(k, 11);
 #ifdef SPDNN_PROFILE
       if (lane == 0) {
         const long long now = clock64();
@@ -1100,6 +1136,8 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     const char *buf = smem + slot * A.buf_bytes;
     mbar_wait(full0 + 8 * slot, phase);  // (launch_layer: never a stale phase)
     const Header h = *reinterpret_cast<const Header *>(buf);
+    if (warp == 0) TRACE(k, 5);
+    if (warp == C - 1) TRACE(k, 8);
     PROF_MARK(0);  // [0] waiting for data
 #ifdef SPDNN_PROFILE
     if (lane == 0 && h.item >= 0) atomicMin(&s_tfirst[slot], (unsigned long long)clock64());
@@ -1129,6 +1167,8 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       // this lane is done with the staged rows: the producer may refill them
       // while the epilogue runs
       mbar_arrive(rfree0 + 8 * slot);
+      if (warp == 0) TRACE(k, 6);
+      if (warp == C - 1) TRACE(k, 9);
       PROF_MARK(1);  // [1] record loop
       // output rows and their biases (staged with the block metadata) are read
       // only now, so they hold no registers across the record loop
@@ -1151,6 +1191,8 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     // every lane arrives (release) after its activity byte store; the
     // publisher warp folds the entry's bytes into the tile once all have
     mbar_arrive(empty0 + 8 * slot);
+    if (warp == 0) TRACE(k, 7);
+    if (warp == C - 1) TRACE(k, 10);
     g += C;
     while (g >= gpi) {
       g -= gpi;
@@ -1560,6 +1602,15 @@ extern "C" int spdnn_profile_read(uint64_t *out, int32_t n, int32_t reset) {
     if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_chain, h, 8 * sizeof(unsigned long long));
     if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   }
+  return SPDNN_OK;
+}
+
+extern "C" int spdnn_trace_read(int64_t *out, int32_t n) {
+  if (!out || n < 0 || n > 96 * 12) return spdnn_fail(SPDNN_EINVAL, "spdnn_trace_read: bad args");
+  long long h[96 * 12];
+  cudaError_t e = cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+  if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
+  for (int i = 0; i < n; i++) out[i] = h[i];
   return SPDNN_OK;
 }
 

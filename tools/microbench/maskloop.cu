@@ -116,6 +116,53 @@ __device__ __forceinline__ void accumulate_mode(u64 *acc, const uint32_t *recs, 
   }
 }
 
+// MODE 4: full-mask records (bit 14 clear) run 14 unpredicated FFMA2;
+// partial records (bit 14 set) carry a jump code in bits 8..11 (prefix
+// rows 0..hi: code hi; suffix rows lo..6: code 5 + lo) and run exactly their
+// rows through a fall-through switch
+__device__ __forceinline__ void rowfma(u64 *acc, const YV &y, float w, int k) {
+  fma2_acc(acc[2 * k], y.v[0], w);
+  fma2_acc(acc[2 * k + 1], y.v[1], w);
+}
+__device__ __forceinline__ void run_record(u64 *acc, uint32_t wd, const YV &y, float w) {
+  if (!(wd & 0x4000u)) {
+#pragma unroll
+    for (int k = 0; k < 7; k++) rowfma(acc, y, w, k);
+    return;
+  }
+  switch ((wd >> 8) & 15u) {
+    case 5: rowfma(acc, y, w, 5);  // fall through
+    case 4: rowfma(acc, y, w, 4);
+    case 3: rowfma(acc, y, w, 3);
+    case 2: rowfma(acc, y, w, 2);
+    case 1: rowfma(acc, y, w, 1);
+    case 0: rowfma(acc, y, w, 0); break;
+    case 6: rowfma(acc, y, w, 1);
+    case 7: rowfma(acc, y, w, 2);
+    case 8: rowfma(acc, y, w, 3);
+    case 9: rowfma(acc, y, w, 4);
+    case 10: rowfma(acc, y, w, 5);
+    case 11: rowfma(acc, y, w, 6); break;
+    default: break;
+  }
+}
+template <int UNROLL>
+__device__ __forceinline__ void accumulate_jump(u64 *acc, const uint32_t *recs, int cnt,
+                                                uint32_t ybase, float w) {
+  const uint4 *rp = reinterpret_cast<const uint4 *>(recs);
+  const uint4 *const end = rp + (cnt >> 2);
+#pragma unroll UNROLL
+  for (; rp < end; rp++) {
+    const uint4 q = *rp;
+    const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+    YV y[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) y[j].load_s(ybase + (wd[j] >> 15));
+#pragma unroll
+    for (int j = 0; j < 4; j++) run_record(acc, wd[j], y[j], w);
+  }
+}
+
 template <int UNROLL, bool PIPE = false, int MODE = 0>
 __global__ void __launch_bounds__(1024, 1)
     loop_kernel(float *out, int reps, int cnt, const float *wp) {
@@ -135,7 +182,15 @@ __global__ void __launch_bounds__(1024, 1)
     uint32_t m = 0;
     for (int k = 0; k < 7; k++)
       if (allfull || (j >= k && j < k + 32)) m |= 2u << k;
-    recs[i] = j < 38 ? ((uint32_t)(7 * g + j) << 24 | m) : 0u;
+    uint32_t code = 0;
+    if (m != 0xfeu && m != 0u) {  // contiguous rows lo..hi: prefix (lo = 0) or suffix (hi = 6)
+      int lo = 0, hi = 6;
+      while (!(m & (2u << lo))) lo++;
+      while (!(m & (2u << hi))) hi--;
+      code = 0x4000u | ((lo == 0 ? (uint32_t)hi : 5u + (uint32_t)lo) << 8);
+    }
+    if (m == 0u) code = 0x4000u | (15u << 8);  // padding word: no rows
+    recs[i] = j < 38 ? ((uint32_t)(7 * g + j) << 24 | m | code) : (0x4000u | (15u << 8));
   }
   for (int i = tid; i < 171 * 128; i += blockDim.x) reinterpret_cast<float *>(ybase)[i] = (i % 7) * 0.25f;
   __syncthreads();
@@ -145,7 +200,8 @@ __global__ void __launch_bounds__(1024, 1)
   const uint32_t *g = recs + (warp % 20) * 40;
   const uint32_t yb = full + 16 * lane;
   for (int rep = 0; rep < reps; rep++) {
-    if (MODE) accumulate_mode<7, MODE>(acc, g, cnt, yb, w);
+    if (MODE == 4) accumulate_jump<UNROLL>(acc, g, cnt, yb, w);
+    else if (MODE) accumulate_mode<7, MODE>(acc, g, cnt, yb, w);
     else if (PIPE) accumulate_mask_pipe<7, UNROLL>(acc, g, cnt, yb, w);
     else accumulate_mask<7, UNROLL>(acc, g, cnt, yb, w);
   }
@@ -187,6 +243,7 @@ int main() {
            name, warps, per_smsp_clk, per_smsp_clk / 0.5);
   };
   for (int warps : {4, 8, 12, 16, 20, 24, 28, 32}) run(loop_kernel<2>, "u2_sliding", warps, 40);
+  for (int warps : {8, 12, 16, 20, 24}) run(loop_kernel<2, false, 4>, "mode4_jump(slots=14/record)", warps, 40);
   for (int warps : {8, 20}) run(loop_kernel<2, false, 1>, "mode1_unpredicated", warps, 40);
   for (int warps : {8, 20}) run(loop_kernel<2, false, 2>, "mode2_no_feature_lds", warps, 40);
   for (int warps : {8, 20}) run(loop_kernel<2, false, 3>, "mode3_no_lds", warps, 40);
