@@ -120,6 +120,16 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_cnt(uint32_t bar, uint32_t cnt) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(bar),
+               "r"(cnt)
+               : "memory");
+}
+// One arrival on `bar` once every cp.async this thread issued so far has landed
+// (the barrier's expected count includes it: .noinc).
+__device__ __forceinline__ void mbar_cp_async_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
 // Blocks (suspended, up to the time hint) until the phase with `parity` is done.
 #ifndef SPDNN_WAIT_TEST
 #define SPDNN_WAIT_TEST 0  // 1: spin on test_wait instead of the suspending try_wait
@@ -736,7 +746,9 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   if (tid == 0) {
     s_wmask = __uint_as_float(A.L.weight_bits);
     for (int i = 0; i < nbuf; i++) {
-      mbar_init(full0 + 8 * i, 1);      // the producer's header arrival (+ tx bytes)
+      // the header arrival + one per producer thread (its row copies landed)
+      // + the tx bytes of the TMA copies
+      mbar_init(full0 + 8 * i, 1 + P * 32);
       mbar_init(empty0 + 8 * i, gpi * 32);  // every lane of every work unit (row group)
       mbar_init(free0 + 8 * i, 32);         // every publisher lane: activity bytes read
       mbar_init(rfree0 + 8 * i, gpi * 32);  // every unit's lanes: staged rows read
@@ -873,7 +885,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
               Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
               h->item = -1;
               h->entry = k;
-              mbar_arrive(full0 + 8 * slot);
+              mbar_arrive_cnt(full0 + 8 * slot, 1 + P * 32);  // (no copies)
             }
             __syncwarp();
           }
@@ -958,15 +970,14 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
           if (4 * qd + 3 >= fp_cnt) c.w = c.x;
           tma_gather4(sy + (uint32_t)qd * 4u * G::kRow, &A.tmap_in, p0, c.x, c.y, c.z, c.w, full);
         }
+        mbar_arrive(full);  // (the bytes complete the phase, not this arrival)
         if (pw == 0) TRACE(k, 1);
         PROF_MARK(6);  // [6] TMA gather4 issue (contiguous tiles)
       } else if (!contig) {
         // staged rows s = 32 pw .. : the warp's 32 lanes copy the row's T
         // features with 4-byte cp.async (tiles whose columns have gaps: the
-        // layer right after one in which features died); every producer
-        // thread waits for its own copies (and the metadata prefetches in
-        // flight), the named barrier below orders all of them before the
-        // header's arrival
+        // layer right after one in which features died); each producer
+        // thread's arrival on the full barrier fires once its copies landed
         for (int s0 = pw * 32; s0 < fp_cnt; s0 += P * 32) {
           const int my = s0 + lane < fp_cnt ? sfp[s0 + lane] : 0;
           const int cnt = min(32, fp_cnt - s0);
@@ -978,9 +989,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
             for (int q = 0; q < FPL; q++) cp_async4(dst + 128 * q, row + max(src[q], 0), src[q] >= 0);
           }
         }
-        cp_async_commit();
-        cp_async_wait<0>();
+        mbar_cp_async_arrive(full);
         PROF_MARK(7);  // [7] 4-byte cp.async gathers (tiles with gaps)
+      } else {
+        mbar_arrive(full);  // (diagnostics build without row staging)
       }
       if (pw == 0) {
         mbar_wait(empty0 + 8 * slot, phase ^ 1u);  // every unit of k - nbuf is done
@@ -993,7 +1005,6 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         mbar_wait(free0 + 8 * slot, phase ^ 1u);  // activity bytes of k - nbuf read
         TRACE(k, 3);
       }
-      if (!contig) pbar();  // every producer's cp.async copies landed
       if (ptid == 0) {
         Header *h = reinterpret_cast<Header *>(smem + slot * A.buf_bytes);
         h->item = item;
