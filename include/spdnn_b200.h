@@ -233,6 +233,11 @@ int spdnn_profile_read(uint64_t *out, int32_t n, int32_t reset);
  * for entry k < 96 (layer.cu, g_trace). n <= 1152. Diagnostics only. */
 int spdnn_trace_read(int64_t *out, int32_t n);
 
+/* Per-launch, per-CTA %globaltimer marks of the last 64 layer launches, when
+ * built with -DSPDNN_LTRACE (layer.cu, g_ltrace): out[(slot*160 + cta)*6 + i],
+ * slot = launch index % 64. n <= 61440. Diagnostics only. */
+int spdnn_ltrace_read(int64_t *out, int32_t n);
+
 /* Threadblocks per SM the layer kernel runs with (for diagnostics). */
 int spdnn_layer_occupancy(int32_t rows_per_group, int32_t *ctas_per_sm,
                           int32_t *threads_per_cta);

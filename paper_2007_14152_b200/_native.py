@@ -116,6 +116,8 @@ def lib():
         L.spdnn_profile_read.restype = ctypes.c_int
         L.spdnn_trace_read.argtypes = [P, i32]
         L.spdnn_trace_read.restype = ctypes.c_int
+        L.spdnn_ltrace_read.argtypes = [P, i32]
+        L.spdnn_ltrace_read.restype = ctypes.c_int
         L.spdnn_last_error.restype = ctypes.c_char_p
         L.spdnn_version.restype = ctypes.c_char_p
         for name in ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
@@ -142,5 +144,6 @@ EXPORTED = ("spdnn_plan_build", "spdnn_plan_build_many", "spdnn_plan_sizes",
             "spdnn_plan_export", "spdnn_plan_free", "spdnn_layer_forward",
             "spdnn_infer_layers", "spdnn_infer_layers_timed", "spdnn_transpose_in",
             "spdnn_gather_out",
-            "spdnn_layer_occupancy", "spdnn_profile_read", "spdnn_trace_read", "spdnn_last_error",
+            "spdnn_layer_occupancy", "spdnn_profile_read", "spdnn_trace_read", "spdnn_ltrace_read",
+            "spdnn_last_error",
             "spdnn_version")

@@ -42,6 +42,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -56,9 +57,16 @@ constexpr int kMaxBufs = 4;
 #define SPDNN_PDL 1  // programmatic dependent launch between consecutive layers
 #endif
 constexpr int kUsePdl = SPDNN_PDL;
-constexpr int kMetaAhead = 5;  // producer: block descriptors prefetched this many items ahead
-constexpr int kFpAhead = 3;    // producer: staged-row lists prefetched this many items ahead
-constexpr int kMetaRing = 7;   // metadata ring entries (> kMetaAhead)
+#ifndef SPDNN_META_AHEAD
+#define SPDNN_META_AHEAD 3
+#endif
+#ifndef SPDNN_FP_AHEAD
+#define SPDNN_FP_AHEAD 2
+#endif
+constexpr int kMetaAhead = SPDNN_META_AHEAD;  // producer: block descriptors prefetched this many items ahead
+constexpr int kFpAhead = SPDNN_FP_AHEAD;      // producer: staged-row lists prefetched this many items ahead (>= 2)
+constexpr int kMetaRing = kMetaAhead + 2;     // metadata ring entries (> kMetaAhead)
+static_assert(kFpAhead >= 2 && kFpAhead < kMetaAhead && kMetaAhead + 2 <= 8, "prefetch depths");
 #ifndef SPDNN_MASK_CONSUMERS
 #define SPDNN_MASK_CONSUMERS 20
 #endif
@@ -232,6 +240,26 @@ __device__ unsigned long long g_chain[8];
 // done, [8]/[9]/[10] the same for the last consumer warp, [11] publisher
 // saw empty; read with spdnn_trace_read()
 __device__ long long g_trace[96][12];
+// per-launch, per-CTA %globaltimer marks (build with -DSPDNN_LTRACE;
+// diagnostics): [0] kernel entry, [1] consumer warp 0 past the grid
+// dependency wait, [2] its first entry's data, [3] its exit, [4] the
+// producer's first slot grant, [5] entries this CTA consumed
+__device__ long long g_ltrace[64][160][6];
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#ifdef SPDNN_LTRACE
+#define LTRACE(i, v)                                                     \
+  do {                                                                  \
+    if (lane == 0 && blockIdx.x < 160) g_ltrace[A.trace_slot & 63][blockIdx.x][(i)] = (v); \
+  } while (0)
+#else
+#define LTRACE(i, v) \
+  do {               \
+  } while (0)
+#endif
 #ifdef SPDNN_TRACE
 #define TRACE(k, i)                                                    \
   do {                                                                 \
@@ -290,6 +318,7 @@ struct LayerArgs {
   uint32_t mentry_bytes;
   int gpi;             // consumer work units (row groups) per item = max groups per block
   uint32_t act_off;    // activity bytes: [nbuf][gpi][32 lanes], one byte per lane and unit
+  int trace_slot;      // SPDNN_LTRACE: row of g_ltrace this launch writes (layer % 64)
 };
 
 // Ring-buffer header written by the producer (one per buffer fill).
@@ -728,6 +757,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   // layer wrote -- m_in, a_in, cat_in, y_in, the tile scratch -- is read only
   // after griddepcontrol.wait (dep_wait below).
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (tid == 0) LTRACE(0, gtime());
   const int nb = (int)A.L.num_blocks;
   int M = 0, tiles = 0, items = 0x7fffffff;  // set by dep_wait
   auto dep_wait = [&]() {
@@ -758,6 +788,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   __syncthreads();
   if (warp < C || warp >= C + P) {
     dep_wait();
+    if (warp == 0) LTRACE(1, gtime());
     if (M <= 0) return;
   }
 
@@ -940,6 +971,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
 #endif
       if (pw == 0) TRACE(k, 0);
+      if (ptid == 0 && k == 0) LTRACE(4, gtime());
       PROF_MARK(0);  // [0] waiting for the slot's rows
       const uint32_t full = full0 + 8 * slot;
       const uint32_t buf = sbase + slot * A.buf_bytes;
@@ -1147,6 +1179,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     const char *buf = smem + slot * A.buf_bytes;
     mbar_wait(full0 + 8 * slot, phase);  // (launch_layer: never a stale phase)
     const Header h = *reinterpret_cast<const Header *>(buf);
+    if (warp == 0 && k == 0) LTRACE(2, gtime());
     if (warp == 0) TRACE(k, 5);
     if (warp == C - 1) TRACE(k, 8);
     PROF_MARK(0);  // [0] waiting for data
@@ -1214,6 +1247,10 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
       }
     }
     PROF_MARK(3);  // [3] unit bookkeeping, tile publishing
+  }
+  if (warp == 0) {
+    LTRACE(3, gtime());
+    LTRACE(5, (long long)k);
   }
   PROF_FLUSH(0)
 }
@@ -1515,6 +1552,10 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   std::memcpy(&tb, &A.tiny, 4);
   A.tiny_bits_m1 = tb ? tb - 1u : 0u;
   A.negz = -0.0f;
+  {
+    static std::atomic<int> launches{0};
+    A.trace_slot = launches.fetch_add(1) & 63;
+  }
   const bool pdl = kUsePdl != 0;
   const bool mask = layer->uniform != 0;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1620,6 +1661,16 @@ extern "C" int spdnn_trace_read(int64_t *out, int32_t n) {
   if (!out || n < 0 || n > 96 * 12) return spdnn_fail(SPDNN_EINVAL, "spdnn_trace_read: bad args");
   long long h[96 * 12];
   cudaError_t e = cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+  if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
+  for (int i = 0; i < n; i++) out[i] = h[i];
+  return SPDNN_OK;
+}
+
+extern "C" int spdnn_ltrace_read(int64_t *out, int32_t n) {
+  if (!out || n < 0 || n > 64 * 160 * 6)
+    return spdnn_fail(SPDNN_EINVAL, "spdnn_ltrace_read: bad args");
+  static long long h[64 * 160 * 6];
+  cudaError_t e = cudaMemcpyFromSymbol(h, g_ltrace, sizeof(h));
   if (e != cudaSuccess) return spdnn_fail(SPDNN_ECUDA, cudaGetErrorString(e));
   for (int i = 0; i < n; i++) out[i] = h[i];
   return SPDNN_OK;
