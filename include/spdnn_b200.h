@@ -159,6 +159,15 @@ typedef struct spdnn_scratch {
   uint32_t *guard;         /* [1] zero-initialised; bit 0 = FMA-form guard
                               tripped (rerun in the exact form), bit 1 =
                               non-finite input (rerun with one row per group) */
+  int32_t *split;          /* optional (NULL: off) [2 * (num_layers + 1)] zero-
+                              initialised: between the layers of one
+                              spdnn_infer_layers call, a tile whose 128 features
+                              all survive is appended as a whole aligned tile and
+                              the other survivors are packed from entry ld on,
+                              so one death does not shift every later tile off
+                              its consecutive columns (the TMA staging path);
+                              the a0/a1/cat0/cat1 buffers must then hold 2 * ld
+                              entries. The last layer's survivors are packed. */
 } spdnn_scratch;
 
 /* Arithmetic form of a launch (layer.cu):

@@ -54,7 +54,7 @@ class LayerDev(ctypes.Structure):
 
 
 class Scratch(ctypes.Structure):
-    _fields_ = [("tile_done", P), ("tile_alive", P), ("work", P), ("guard", P)]
+    _fields_ = [("tile_done", P), ("tile_alive", P), ("work", P), ("guard", P), ("split", P)]
 
 
 class RunOpts(ctypes.Structure):

@@ -300,6 +300,13 @@ struct LayerArgs {
   const int32_t *a_in;
   const int64_t *cat_in;
   const int32_t *m_in;
+  // split survivor layout (scratch->split): al_in[0] = how many leading input
+  // features form whole tiles of consecutive columns (the rest start at
+  // a_in / cat_in + pk_off); al_out: the same counters for this layer's
+  // survivors (aligned, packed), NULL = the packed layout
+  const int32_t *al_in;
+  int32_t *al_out;
+  int64_t pk_off;
   int32_t *a_out;
   int64_t *cat_out;
   int32_t *m_out;
@@ -689,6 +696,7 @@ __device__ __forceinline__ void epilogue(const LayerArgs &A, u64 *acc, const int
 template <int R, bool FMA, int FPL, bool MASK>
 __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, int lane, int M,
                                   u64 negz2) {
+  const int nal = A.al_in ? *A.al_in : 0x7fffffff;
   constexpr int RW = MASK ? 1 : Rec<R>::W, H = FPL / 2, T = Geo<FPL>::kTileF;
   const float w0 = __uint_as_float(A.L.weight_bits);
   const int nst = __ldg(A.L.blocks + (int64_t)b * 8 + 2);
@@ -699,7 +707,7 @@ __device__ void accumulate_global(const LayerArgs &A, u64 *acc, int b, int t, in
   for (int q = 0; q < FPL; q++) {
     const int j = t * T + FPL * lane + q;
     ok[q] = j < M;
-    pos[q] = ok[q] ? __ldg(A.a_in + j) : 0;
+    pos[q] = ok[q] ? __ldg(A.a_in + (A.al_in && j >= nal ? A.pk_off + (j - nal) : (int64_t)j)) : 0;
   }
   for (int s = 1; s < nst; s++) {
     const int4 sd = __ldg(reinterpret_cast<const int4 *>(A.L.stages) + first_extra + s - 1);
@@ -760,9 +768,14 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   if (tid == 0) LTRACE(0, gtime());
   const int nb = (int)A.L.num_blocks;
   int M = 0, tiles = 0, items = 0x7fffffff;  // set by dep_wait
+  int nal = 0x7fffffff;  // input features [0, nal) sit at their own index in a_in / cat_in
+  // where input feature j's column and category are (split layout: the
+  // aligned tiles, then the packed survivors at pk_off)
+  auto pos = [&](int j) -> int64_t { return j < nal ? (int64_t)j : A.pk_off + (j - nal); };
   auto dep_wait = [&]() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     M = *A.m_in;
+    if (A.al_in) nal = *A.al_in;
     tiles = (M + T - 1) / T;
     items = tiles * nb;
   };
@@ -834,7 +847,7 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         if (blk) cp_async16(e + 16 * ptid, A.L.blocks + (int64_t)b * 8 + 4 * ptid);
       } else if (ptid < 2 + T / 4) {
         const int q = ptid - 2;  // a_in has ld >= (t+1)*T entries; lanes past M are masked
-        if (ain) cp_async16(e + 32 + 16 * q, A.a_in + t * T + 4 * q);
+        if (ain) cp_async16(e + 32 + 16 * q, A.a_in + pos(t * T) + 4 * q);
       }
     };
     auto prefetch_fp = [&](int j) {  // staged-row list of item j (descriptor landed)
@@ -889,6 +902,18 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
     if (M <= 0) {
       cp_async_wait<0>();
       return;
+    }
+    if (A.al_in) {  // split input: a first tile among the packed survivors is refetched
+      cp_async_wait<0>();  // (after the speculative copies: cp.async copies are unordered)
+      for (int j = 0; j < kMetaAhead; j++) {
+        const int t0 = tile_of(item_of(j));
+        if (t0 * T >= nal && t0 < tiles) {
+          const uint32_t e = (uint32_t)__cvta_generic_to_shared(ment(j));
+          if (ptid >= 2 && ptid < 2 + T / 4)
+            cp_async16(e + 32 + 16 * (ptid - 2), A.a_in + pos(t0 * T) + 4 * (ptid - 2));
+        }
+      }
+      cp_async_commit();
     }
     cp_async_wait<0>();
     pbar();
@@ -1099,17 +1124,26 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
         tot += __popc(mw[q]);
         below += __popc(mw[q] & ((1u << lane) - 1u));  // alive features of lanes < this
       }
-      int base = 0;
-      if (lane == 0 && tot) base = atomicAdd(A.m_out, tot);
+      // split layout: a whole tile of survivors is appended as an aligned
+      // tile (its columns stay consecutive: the next layer stages it with
+      // TMA gather4 even after deaths elsewhere); other survivors are packed
+      const bool whole = A.al_out && tot == T && (t + 1) * T <= M;
+      int64_t base = 0;
+      if (lane == 0 && tot) {
+        const int old = atomicAdd(A.m_out, tot);  // the layer's survivor count
+        if (!A.al_out) base = old;
+        else if (whole) base = atomicAdd(A.al_out, T);
+        else base = A.pk_off + atomicAdd(A.al_out + 1, tot);
+      }
       base = __shfl_sync(0xffffffffu, base, 0);
       // this lane's features FPL*lane + q, in feature order
-      int rank = base + below;
+      int64_t rank = base + below;
 #pragma unroll
       for (int q = 0; q < FPL; q++) {
         if ((mw[q] >> lane) & 1u) {
           const int j = t * T + FPL * lane + q;
           A.a_out[rank] = j;
-          A.cat_out[rank] = A.cat_in[j];
+          A.cat_out[rank] = A.cat_in[pos(j)];
           rank++;
         }
       }
@@ -1516,7 +1550,8 @@ int tensor_map_for(const float *y, int64_t n, int64_t ld, int box_cols, CUtensor
 int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, float *y_out,
             int64_t ld, const int32_t *a_in, const int64_t *cat_in, const int32_t *m_in,
             int32_t *a_out, int64_t *cat_out, int32_t *m_out, const spdnn_scratch *scratch,
-            int32_t *work, const spdnn_run_opts *opts, void *stream) {
+            int32_t *work, const spdnn_run_opts *opts, void *stream,
+            const int32_t *al_in = nullptr, int32_t *al_out = nullptr) {
   // ld * 4 must fit 32 bits: the epilogue forms row addresses with one wide multiply
   if (!layer || !bias || !y_in || !y_out || !a_in || !cat_in || !m_in || !a_out ||
       !cat_out || !m_out || !scratch || !work || ld < 1 || ld % SPDNN_TILE_FEATURES ||
@@ -1543,6 +1578,9 @@ int forward(const spdnn_layer_dev *layer, const float *bias, const float *y_in, 
   A.a_out = a_out;
   A.cat_out = cat_out;
   A.m_out = m_out;
+  A.al_in = al_in;
+  A.al_out = al_out;
+  A.pk_off = ld;  // split layout: a_* / cat_* hold 2 * ld entries
   A.tile_done = scratch->tile_done;
   A.tile_alive = scratch->tile_alive;
   A.work = work;
@@ -1590,8 +1628,13 @@ static int infer_layers(int64_t num_layers, const spdnn_layer_dev *layers, const
     int64_t *cat[2] = {cat0, cat1};
     if (events && cudaEventRecord((cudaEvent_t)events[l], (cudaStream_t)stream) != cudaSuccess)
       return spdnn_fail(SPDNN_ECUDA, "spdnn_infer_layers_timed: event record failed");
+    // split survivor layout between the layers of this call (scratch->split);
+    // the last layer's survivors are packed, as spdnn_infer_layers returns them
+    int32_t *sp = scratch->split;
+    const int32_t *al_in = sp && l > 0 ? sp + 2 * l : nullptr;
+    int32_t *al_out = sp && l + 1 < num_layers ? sp + 2 * (l + 1) : nullptr;
     int rc = forward(&layers[l], bias, y[i], y[o], ld, a[i], cat[i], counts + l, a[o], cat[o],
-                     counts + l + 1, scratch, scratch->work + l, opts, stream);
+                     counts + l + 1, scratch, scratch->work + l, opts, stream, al_in, al_out);
     if (rc) return rc;
   }
   if (events && cudaEventRecord((cudaEvent_t)events[num_layers], (cudaStream_t)stream) !=

@@ -457,6 +457,11 @@ class DeviceNetwork:
         self.huge = float(np.ldexp(1.0, min(127, 95 - emax))) if emax < 95 else 0.0
 
 
+# whole surviving tiles stay aligned between layers (spdnn_scratch.split);
+# SPDNN_SPLIT=0 packs every layer's survivors (diagnostics)
+SPLIT_LAYOUT = __import__("os").environ.get("SPDNN_SPLIT", "1") != "0"
+
+
 class Workspace:
     """Per-inference device buffers for a feature-count capacity (reused)."""
 
@@ -470,15 +475,18 @@ class Workspace:
         self.x = torch.empty((m_cap, neurons), dtype=f32, device=device)  # raw upload
         nb = range(buffers)
         self.y = [torch.empty((neurons, self.ld), dtype=f32, device=device) for _ in nb]
-        self.a = [torch.empty(self.ld, dtype=i32, device=device) for _ in nb]
-        self.cat = [torch.empty(self.ld, dtype=i64, device=device) for _ in nb]
+        # 2 * ld entries: the split survivor layout between layers (spdnn_scratch.split)
+        self.a = [torch.empty(2 * self.ld, dtype=i32, device=device) for _ in nb]
+        self.cat = [torch.empty(2 * self.ld, dtype=i64, device=device) for _ in nb]
         self.counts = torch.zeros(num_layers + 1, dtype=i32, device=device)
         self.tile_done = torch.zeros(self.ld // 64, dtype=i32, device=device)
         self.tile_alive = torch.zeros(self.ld // 32, dtype=i32, device=device)
         self.work = torch.zeros(max(1, num_layers), dtype=i32, device=device)
         self.guard = torch.zeros(1, dtype=i32, device=device)
+        self.split = torch.zeros(2 * (max(1, num_layers) + 1), dtype=i32, device=device)
         self.scratch = _native.Scratch(self.tile_done.data_ptr(), self.tile_alive.data_ptr(),
-                                       self.work.data_ptr(), self.guard.data_ptr())
+                                       self.work.data_ptr(), self.guard.data_ptr(),
+                                       self.split.data_ptr() if SPLIT_LAYOUT else None)
         self.iota = torch.arange(self.ld, dtype=i32, device=device)
 
     def fits(self, neurons: int, m: int, num_layers: int) -> bool:
@@ -580,6 +588,7 @@ def reset_run(ws: Workspace, m0: int) -> None:
     ws.counts.zero_()
     ws.counts[0] = m0
     ws.work.zero_()
+    ws.split.zero_()
 
 
 def run_layers(net: DeviceNetwork, ws: Workspace, m0: int, fma: bool | None = None
