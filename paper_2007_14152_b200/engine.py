@@ -788,9 +788,10 @@ class _PipeBuffers:
         self.ws = Workspace(n, cap, num_layers, device)  # y[0..1], scratch, iota
         self.x = [self.ws.x, torch.empty((cap, n), dtype=torch.float32, device=device)]
         i32, i64 = torch.int32, torch.int64
-        self.a = [[torch.empty(self.ws.ld, dtype=i32, device=device) for _ in range(2)]
+        # 2 * ld entries: the split survivor layout between layers
+        self.a = [[torch.empty(2 * self.ws.ld, dtype=i32, device=device) for _ in range(2)]
                   for _ in range(chunks)]
-        self.cat = [[torch.empty(self.ws.ld, dtype=i64, device=device) for _ in range(2)]
+        self.cat = [[torch.empty(2 * self.ws.ld, dtype=i64, device=device) for _ in range(2)]
                     for _ in range(chunks)]
         self.counts = torch.zeros((chunks, num_layers + 1), dtype=i32, device=device)
         self.guard = torch.zeros(chunks, dtype=i32, device=device)
@@ -858,8 +859,10 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
         cnt.zero_()
         cnt[0] = mc
         ws.work.zero_()
+        ws.split.zero_()
         sc = _native.Scratch(ws.tile_done.data_ptr(), ws.tile_alive.data_ptr(),
-                             ws.work.data_ptr(), pb.guard.data_ptr() + 4 * c)
+                             ws.work.data_ptr(), pb.guard.data_ptr() + 4 * c,
+                             ws.split.data_ptr() if SPLIT_LAYOUT else None)
         _native.check(lib.spdnn_infer_layers(
             L, net.layer_devs, _dptr(net.bias), _dptr(ws.y[0]), _dptr(ws.y[1]), ws.ld,
             _dptr(pb.a[c][0]), _dptr(pb.a[c][1]), _dptr(pb.cat[c][0]), _dptr(pb.cat[c][1]),
