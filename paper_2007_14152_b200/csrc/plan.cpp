@@ -89,14 +89,16 @@ bool valid_csr(int64_t n, const int64_t *rp, const int32_t *ci) {
 // column, restart at the lowest unvisited row. Columns feeding more than
 // `deg_cap` rows are skipped as candidate generators (bounded cost on dense
 // columns; they still count toward nothing else).
-std::vector<int32_t> overlap_order(int64_t n, const int64_t *rp, const int32_t *ci) {
+// (n rows over ncol columns)
+std::vector<int32_t> overlap_order_cols(int64_t n, int64_t ncol, const int64_t *rp,
+                                        const int32_t *ci) {
   std::vector<int32_t> order;
   order.reserve(n);
   if (n == 0) return order;
   // column -> rows (CSC pattern)
-  std::vector<int64_t> cp(n + 1, 0);
+  std::vector<int64_t> cp(ncol + 1, 0);
   for (int64_t p = 0; p < rp[n]; p++) cp[ci[p] + 1]++;
-  for (int64_t c = 0; c < n; c++) cp[c + 1] += cp[c];
+  for (int64_t c = 0; c < ncol; c++) cp[c + 1] += cp[c];
   std::vector<int32_t> cr(rp[n]);
   {
     std::vector<int64_t> fill(cp.begin(), cp.end() - 1);
@@ -136,6 +138,78 @@ std::vector<int32_t> overlap_order(int64_t n, const int64_t *rp, const int32_t *
     touched.clear();
     cur = best;
   }
+  return order;
+}
+
+std::vector<int32_t> overlap_order(int64_t n, const int64_t *rp, const int32_t *ci) {
+  return overlap_order_cols(n, n, rp, ci);
+}
+
+// overlap_order over classes of identical rows: rows with the same column
+// list (e.g. 2^v rows per window when the generator's offset/stride ratio has
+// 2-adic valuation v) form one class; the greedy chain runs over one
+// representative per class and each class is emitted in place, so a row
+// group falls inside one class (its union is the rows' own columns: no
+// padding). Without this, a column shared by more than deg_cap identical rows
+// is skipped as a generator and the chain degrades to the identity order.
+std::vector<int32_t> class_overlap_order(int64_t n, const int64_t *rp, const int32_t *ci) {
+  std::vector<uint64_t> h((size_t)n);
+  for (int64_t r = 0; r < n; r++) {
+    uint64_t x = 1469598103934665603ull ^ (uint64_t)(rp[r + 1] - rp[r]);
+    for (int64_t p = rp[r]; p < rp[r + 1]; p++) x = (x ^ (uint64_t)(uint32_t)ci[p]) * 1099511628211ull;
+    h[(size_t)r] = x;
+  }
+  std::vector<int32_t> idx((size_t)n);
+  for (int64_t r = 0; r < n; r++) idx[(size_t)r] = (int32_t)r;
+  std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) { return h[a] < h[b]; });
+  auto same = [&](int32_t a, int32_t b) {
+    const int64_t la = rp[a + 1] - rp[a];
+    return la == rp[b + 1] - rp[b] && std::equal(ci + rp[a], ci + rp[a] + la, ci + rp[b]);
+  };
+  // classes: members listed in ascending row index, representative = first
+  std::vector<int32_t> cls_of((size_t)n, -1), reps;
+  std::vector<std::vector<int32_t>> members;
+  for (size_t i = 0; i < idx.size();) {
+    size_t j = i;
+    while (j < idx.size() && h[idx[j]] == h[idx[i]]) j++;
+    // rows with equal hashes: split into classes of equal column lists
+    for (size_t a = i; a < j; a++) {
+      const int32_t r = idx[a];
+      if (cls_of[r] >= 0) continue;
+      const int32_t c = (int32_t)reps.size();
+      reps.push_back(r);
+      members.emplace_back();
+      for (size_t b = a; b < j; b++)
+        if (cls_of[idx[b]] < 0 && same(r, idx[b])) {
+          cls_of[idx[b]] = c;
+          members.back().push_back(idx[b]);
+        }
+    }
+    i = j;
+  }
+  if ((int64_t)reps.size() == n) return overlap_order(n, rp, ci);
+  // the representatives as a CSR, ordered by their smallest member row
+  std::vector<int32_t> cord((size_t)reps.size());
+  for (size_t c = 0; c < reps.size(); c++) {
+    std::sort(members[c].begin(), members[c].end());
+    cord[c] = (int32_t)c;
+  }
+  std::sort(cord.begin(), cord.end(),
+            [&](int32_t a, int32_t b) { return members[a][0] < members[b][0]; });
+  const int64_t nc = (int64_t)reps.size();
+  std::vector<int64_t> rp2((size_t)nc + 1, 0);
+  std::vector<int32_t> ci2;
+  for (int64_t k = 0; k < nc; k++) {
+    const int32_t r = reps[cord[k]];
+    ci2.insert(ci2.end(), ci + rp[r], ci + rp[r + 1]);
+    rp2[(size_t)k + 1] = (int64_t)ci2.size();
+  }
+  // column ids stay < n; the chain only compares column sets
+  std::vector<int32_t> corder = overlap_order_cols(nc, n, rp2.data(), ci2.data());
+  std::vector<int32_t> order;
+  order.reserve((size_t)n);
+  for (int32_t k : corder)
+    for (int32_t r : members[cord[k]]) order.push_back(r);
   return order;
 }
 
@@ -406,7 +480,7 @@ extern "C" int spdnn_plan_build(int64_t n, const int64_t *row_ptr, const int32_t
       R = 1;
       best = make_groups(n, row_ptr, col_idx, ident, 1);
     } else {
-      std::vector<int32_t> order = p.reorder ? overlap_order(n, row_ptr, col_idx) : ident;
+      std::vector<int32_t> order = p.reorder ? class_overlap_order(n, row_ptr, col_idx) : ident;
       if (R != 0) {
         best = make_groups(n, row_ptr, col_idx, order, R);
       } else {
