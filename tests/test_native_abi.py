@@ -34,3 +34,23 @@ def test_error_path_sets_message():
     rc = lib.spdnn_plan_sizes(None, None)
     assert rc == _native.SPDNN_EINVAL
     assert b"null" in lib.spdnn_last_error()
+
+
+def _header_struct_fields(name):
+    """Field names of `typedef struct name {...} name;` in the header."""
+    text = open(os.path.join(_native.INCLUDE, "spdnn_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    body = re.search(r"typedef struct %s(?:_t)?\s*\{(.*?)\}\s*%s;" % (name.rstrip("_t"), name),
+                     text, flags=re.S)
+    assert body, name
+    return [m.group(1) for m in re.finditer(r"[\w\s\*]+?\b(\w+)\s*;", body.group(1))]
+
+
+def test_ctypes_structs_match_the_header():
+    """The Python side's ctypes mirrors of the ABI structs list the header's
+    fields in the header's order (a mismatch would shift every later field)."""
+    pairs = [("spdnn_plan_params", _native.PlanParams), ("spdnn_plan_sizes_t", _native.PlanSizes),
+             ("spdnn_layer_dev", _native.LayerDev), ("spdnn_scratch", _native.Scratch),
+             ("spdnn_run_opts", _native.RunOpts)]
+    for cname, py in pairs:
+        assert _header_struct_fields(cname) == [f[0] for f in py._fields_], cname
