@@ -102,6 +102,36 @@ def test_sliding_window_layers_group_well():
         assert plan.num_fp / 4096 < 1.35
 
 
+def test_identical_rows_form_classes():
+    """Windows shared by thousands of rows (offset/stride ratio with 2-adic
+    valuation >= 10 in the generator; each column fans out to > 512 rows):
+    identical rows are grouped before the overlap chain, so every row group
+    lies inside one class -- R = 7 with (almost) no union padding instead of
+    the R = 1 fallback the plain chain produced -- and the layout stays
+    bit-exact, including classes mixed with distinct rows."""
+    n, k, v = 4096, 32, 10
+    r = np.arange(n)
+    starts = (r * (1 << v)) % n                    # 2^v rows per window start
+    cols = (starts[:, None] + np.arange(k)[None, :]) % n
+    layer = make_layer_csr(n, np.repeat(r, k), cols.reshape(-1),
+                           np.full(n * k, 0.0625, np.float32))
+    plan = build_plans([layer], PlanParams())[0]
+    assert plan.rows_per_group == 7
+    assert n * k / plan.padded_slots > 0.98
+    rng = np.random.default_rng(11)
+    _check(layer, PlanParams(), rng, m=4)
+    # classes of several sizes next to unique rows
+    m_rows = 300
+    base = rng.integers(0, 200, m_rows) % 7          # 7 distinct windows, uneven classes
+    uniq = np.arange(m_rows) % 3 == 0                 # every third row its own window
+    st = np.where(uniq, 40 + np.arange(m_rows), base * 5)
+    cl = (st[:, None] + np.arange(6)[None, :]) % m_rows
+    mixed = make_layer_csr(m_rows, np.repeat(np.arange(m_rows), 6), cl.reshape(-1),
+                           rng.uniform(-1, 1, m_rows * 6).astype(np.float32))
+    for p in PARAMS:
+        _check(mixed, p, rng)
+
+
 def test_empty_and_degenerate_layers():
     rng = np.random.default_rng(9)
     empty = make_layer_csr(5, np.empty(0), np.empty(0), np.empty(0, np.float32))
