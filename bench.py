@@ -482,6 +482,11 @@ def run_ours_multi(args, cfg):
             "roofline": {"bound": "hbm", "achieved": bytes_total / (ms / 1e3) / 1e9,
                          "peak": peak, "unit": "GB/s",
                          "frac": bytes_total / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "traffic_single_gpu": ncu_traffic(args.config)[0],
+                         "traffic_single_gpu_source": (
+                             "profiles/%s: DRAM read+write of one steady launch of the same "
+                             "kernel on the whole batch (one GPU); a rank's launch moves its "
+                             "shard's share" % ncu_traffic(args.config)[1]),
                          "peak_source": peak_src,
                          "note": "per-GPU algorithmic bytes over the whole step (count "
                                  "exchange, one allgather per layer window, included)"},
@@ -548,8 +553,12 @@ def resident_workload(args, cfg, params):
         return {"sample_columns": int(n_s), "survivors_in_sample": int(len(sample["categories"])),
                 "bit_exact": bool(np.array_equal(got, sample["categories"]))}
 
+    def e2e_variant(batch, values):
+        return engine.infer(model, batch, InferenceConfig(), prepared=prepared, values=values)
+
     return Workload(net=net, nnz=np.array([l.nnz for l in model.layers], np.float64),
                     e2e=e2e, e2e_path="engine.infer(values=False) on a pinned-host FeatureBatch",
+                    e2e_variant=e2e_variant,
                     cpu=cpu, parity=parity, parity_after_cpu=True)
 
 
@@ -758,6 +767,27 @@ def run_ours(args, cfg):
     assert np.array_equal(res.categories, cats_chk.cpu().numpy()), "e2e categories differ"
     h2d = m * n * 4 + m * 8
     d2h = len(res.categories) * 8 + (L + 1) * 4
+    # the same call as a reference caller makes it: a pageable numpy batch,
+    # and with the final values copied back (engine.infer's default)
+    variants = None
+    if getattr(W, "e2e_variant", None) is not None:
+        from paper_2007_14152_b200.model import make_feature_batch
+        pageable = make_feature_batch(n, np.array(batch.data, order="F"), batch.categories)
+        variants = {}
+        for key, b_, vals in (("pageable_values_false", pageable, False),
+                              ("pinned_values_true", batch, True)):
+            r_ = W.e2e_variant(b_, vals)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r_ = W.e2e_variant(b_, vals)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            assert np.array_equal(r_.categories, res.categories), key
+            variants[key] = {"value": edges_step / dt / 1e12, "unit": "TE/s",
+                             "ms_per_step": dt * 1e3,
+                             "d2h_bytes_per_step": d2h + (len(r_.categories) * n * 4
+                                                          if vals else 0)}
+        del pageable
     parity = W.parity(res.categories) if W.parity and not W.parity_after_cpu else None
     cpu = W.cpu(batch) if args.cpu_sample > 0 else None
     if W.parity and W.parity_after_cpu:
@@ -782,7 +812,8 @@ def run_ours(args, cfg):
                    "layout_hbm_gb": round(net.hbm_bytes / 1e9, 2)},
         "e2e": {"value": edges_step / e2e_s / 1e12, "unit": "TE/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_s * 1e3, "path": W.e2e_path},
+                "ms_per_step": e2e_s * 1e3, "path": W.e2e_path,
+                "variants": variants},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "traffic_source": (f"profiles/{traffic_src}: dram read+write of one "

@@ -498,20 +498,31 @@ _net_cache: dict = {}
 _ws_cache: dict = {}
 
 
+# resident networks kept for repeated or alternating infer calls: least
+# recently used first out, at most this many or this share of device memory
+NET_CACHE_MAX = 4
+NET_CACHE_HBM_SHARE = 0.25
+
+
 def device_network(prepared: Sequence[PreparedLayer], bias: np.ndarray) -> DeviceNetwork:
-    """Upload (once) and cache the device copy of a prepared model. One
-    network stays resident per process: a new one evicts the previous."""
+    """Upload (once) and cache the device copy of a prepared model. Up to
+    NET_CACHE_MAX networks stay resident per process (least recently used is
+    evicted first, and beyond NET_CACHE_HBM_SHARE of device memory), so
+    alternating infer calls on two models do not re-upload either."""
     torch = _torch()
     dev = torch.cuda.current_device()
     with _cache_lock:
-        hit = _net_cache.get("net")
-        if hit is not None:
-            c_prep, c_bias, c_dev, net = hit
+        nets = _net_cache.setdefault("nets", [])  # [(prepared, bias, dev, net)], MRU last
+        for i, (c_prep, c_bias, c_dev, net) in enumerate(nets):
             if c_prep is prepared and c_dev == dev and np.array_equal(c_bias, bias):
+                nets.append(nets.pop(i))
                 return net
-        _net_cache.clear()
         net = DeviceNetwork(prepared, bias)
-        _net_cache["net"] = (prepared, np.array(bias, copy=True), dev, net)
+        nets.append((prepared, np.array(bias, copy=True), dev, net))
+        budget = NET_CACHE_HBM_SHARE * torch.cuda.get_device_properties(dev).total_memory
+        while len(nets) > 1 and (len(nets) > NET_CACHE_MAX or
+                                 sum(e[3].hbm_bytes for e in nets) > budget):
+            nets.pop(0)
         return net
 
 

@@ -471,3 +471,27 @@ def test_randomized_structured_networks(cuda_ok):
         assert [o.active_before for o in res.per_layer] + [len(res.categories)] == \
             ref.counts.tolist(), msg
         assert same_bits(res.final.data, ref.final), msg
+
+
+def test_alternating_models_keep_their_device_networks(cuda_ok):
+    """Two prepared models used in turn stay resident (LRU network cache):
+    the second call on a model reuses its uploaded layout, and both models'
+    results stay bit-exact against the oracle."""
+    mk = lambda seed, n: ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=n, layers=6, connections_per_neuron=16, bias_value=-0.2, seed=seed))
+    ma, mb = mk(31, 512), mk(32, 256)
+    pa = engine.prepare_model(ma, InferenceConfig(), "optimized")
+    pb = engine.prepare_model(mb, InferenceConfig(), "optimized")
+    ia = ingest.generate_synthetic_inputs(512, 300, 0.3, seed=5)
+    ib = ingest.generate_synthetic_inputs(256, 300, 0.3, seed=6)
+    net_a = engine.device_network(pa, ma.bias)
+    net_b = engine.device_network(pb, mb.bias)
+    assert engine.device_network(pa, ma.bias) is net_a
+    assert engine.device_network(pb, mb.bias) is net_b
+    for model, prep, inputs in ((ma, pa, ia), (mb, pb, ib), (ma, pa, ia)):
+        res = engine.infer(model, inputs, InferenceConfig(), prepared=prep)
+        ref = oracle.infer(model, inputs, threads=4)
+        assert np.array_equal(res.categories, ref.categories)
+        assert np.array_equal(np.asarray(res.final.data).view(np.uint32),
+                              np.asarray(ref.final).view(np.uint32))
+    assert engine.device_network(pa, ma.bias) is net_a
