@@ -294,6 +294,99 @@ def host_tensor(a: np.ndarray):
         return torch.from_numpy(a)
 
 
+# ---------------------------------------------------------------------------
+# host <-> device copies of pageable numpy memory (a reference caller's
+# FeatureBatch, the returned final values): the driver's pageable path runs at
+# ~2 GB/s into fresh memory (first-touch page faults inside the copy); here the
+# bytes go through two reused pinned chunks, the CPU side copied by a few
+# threads (page faults in parallel) while the DMA of the other chunk runs.
+
+STAGE_CHUNK = 32 << 20
+_STAGE_THREADS = 8
+_stage_lock = threading.Lock()
+_stage: dict = {}
+
+
+def _stage_buffers(torch, dev):
+    with _stage_lock:
+        st = _stage.get(dev)
+        if st is None:
+            bufs = [torch.empty(STAGE_CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+            from concurrent.futures import ThreadPoolExecutor
+            st = (bufs, [b.numpy() for b in bufs], ThreadPoolExecutor(_STAGE_THREADS))
+            _stage[dev] = st
+        return st
+
+
+def _par_copy(pool, dst: np.ndarray, src: np.ndarray) -> None:
+    """dst[:] = src (flat uint8 views) split over the pool's threads."""
+    n = dst.size
+    parts = min(_STAGE_THREADS, max(1, n >> 22))
+    step = -(-n // parts)
+    futs = [pool.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, n, step)]
+    for f in futs:
+        f.result()
+
+
+def d2h_numpy(src) -> np.ndarray:
+    """A contiguous device tensor as a new (pageable) numpy array, through the
+    pinned chunks (D2H of chunk i+1 overlaps the CPU copy of chunk i)."""
+    torch = _torch()
+    src = src.contiguous()
+    out = np.empty(tuple(src.shape), dtype=np.dtype(str(src.dtype).replace("torch.", "")))
+    nbytes = out.nbytes
+    if nbytes < (4 << 20):
+        out[...] = src.cpu().numpy()
+        return out
+    bufs, views, pool = _stage_buffers(torch, src.device.index)
+    s8 = src.reshape(-1).view(torch.uint8)
+    o8 = out.reshape(-1).view(np.uint8)
+    stream = torch.cuda.current_stream()
+    events = [torch.cuda.Event(), torch.cuda.Event()]
+    pending = None  # (buffer index, offset, length) copied to the GPU, not yet to `out`
+    for i, off in enumerate(range(0, nbytes, STAGE_CHUNK)):
+        b, ln = i % 2, min(STAGE_CHUNK, nbytes - off)
+        bufs[b][:ln].copy_(s8[off:off + ln], non_blocking=True)
+        events[b].record(stream)
+        if pending is not None:
+            pb_, poff, pln = pending
+            events[pb_].synchronize()
+            _par_copy(pool, o8[poff:poff + pln], views[pb_][:pln])
+        pending = (b, off, ln)
+    pb_, poff, pln = pending
+    events[pb_].synchronize()
+    _par_copy(pool, o8[poff:poff + pln], views[pb_][:pln])
+    return out
+
+
+def h2d_into(dst, src: np.ndarray) -> None:
+    """dst (contiguous device tensor) <- src (C-contiguous host array of the
+    same byte size), through the pinned chunks when src is pageable; pinned
+    sources are copied directly. Stream-ordered on the current stream; returns
+    once every source byte has been handed to a copy."""
+    torch = _torch()
+    t = host_tensor(src)
+    if t.is_pinned() or src.nbytes < (4 << 20):
+        dst.copy_(t.reshape(dst.shape), non_blocking=True)
+        return
+    bufs, views, pool = _stage_buffers(torch, dst.device.index)
+    d8 = dst.reshape(-1).view(torch.uint8)
+    s8 = src.reshape(-1).view(np.uint8)
+    stream = torch.cuda.current_stream()
+    events = [None, None]
+    for i, off in enumerate(range(0, src.nbytes, STAGE_CHUNK)):
+        b, ln = i % 2, min(STAGE_CHUNK, src.nbytes - off)
+        if events[b] is not None:
+            events[b].synchronize()  # the chunk that used this buffer has been copied
+        _par_copy(pool, views[b][:ln], s8[off:off + ln])
+        d8[off:off + ln].copy_(bufs[b][:ln], non_blocking=True)
+        events[b] = torch.cuda.Event()
+        events[b].record(stream)
+    for e in events:
+        if e is not None:
+            e.synchronize()
+
+
 def _dptr(t) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
 
@@ -574,7 +667,10 @@ def stage_inputs(ws: Workspace, x_host_or_dev, categories, net: "DeviceNetwork |
     n = ws.neurons
     ws.guard.zero_()
     if m:
-        ws.x[:m].copy_(x_host_or_dev, non_blocking=True)
+        if isinstance(x_host_or_dev, np.ndarray):
+            h2d_into(ws.x[:m], x_host_or_dev)
+        else:
+            ws.x[:m].copy_(x_host_or_dev, non_blocking=True)
         tiny = net.tiny if net is not None else 0.0
         huge = net.huge if net is not None else 3.0e38
         _native.check(_native.lib().spdnn_transpose_in(
@@ -725,7 +821,7 @@ def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
     if net.num_layers == 0 or m == 0:
         return _trivial_result(net.num_layers, inputs, edges // max(inputs.total_inputs, 1))
     ws = workspace(n, m, net.num_layers)
-    x = host_tensor(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
+    x = np.asarray(inputs.data).T  # (M, N) C-order view of the Fortran bytes
     cats = host_tensor(np.ascontiguousarray(inputs.categories))
     fma = None
     elapsed = device = 0.0
@@ -758,7 +854,7 @@ def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
     cats_np = sorted_cats.cpu().numpy().astype(np.int64)
     final = None
     if values:
-        final = FeatureBatch(neurons=n, data=vals.cpu().numpy().T, categories=cats_np,
+        final = FeatureBatch(neurons=n, data=d2h_numpy(vals).T, categories=cats_np,
                              total_inputs=inputs.total_inputs)
     return InferenceResult(final=final, categories=cats_np.copy(),
                            per_layer=_outcomes(counts, net), elapsed_seconds=elapsed,
@@ -836,7 +932,7 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
             pb = _PipeBuffers(n, cap, chunks, L, torch.device("cuda", dev))
             _pipe_cache[key] = pb
     ws = pb.ws
-    host = host_tensor(np.asarray(inputs.data).T)  # (M, N) view of the Fortran bytes
+    host = np.asarray(inputs.data).T  # (M, N) C-order view of the Fortran bytes
     cats = host_tensor(np.ascontiguousarray(inputs.categories))
     main, up = torch.cuda.current_stream(), pb.up
     lib = _native.lib()
@@ -852,7 +948,7 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
         with torch.cuda.stream(up):
             if freed[c % 2] is not None:
                 up.wait_event(freed[c % 2])  # chunk c-2 has been laid out
-            xb[:mc].copy_(host[lo:hi], non_blocking=True)
+            h2d_into(xb[:mc], host[lo:hi])  # (pageable sources: staged, blocking)
             pb.cat[c][0][:mc].copy_(cats[lo:hi], non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(up)
@@ -1057,7 +1153,7 @@ def _infer_streaming(model: NetworkModel, inputs: FeatureBatch, config: Inferenc
     cats_np = sorted_cats.cpu().numpy().astype(np.int64)
     final = None
     if values:
-        final = FeatureBatch(neurons=n, data=vals.cpu().numpy().T, categories=cats_np,
+        final = FeatureBatch(neurons=n, data=d2h_numpy(vals).T, categories=cats_np,
                              total_inputs=inputs.total_inputs)
     return InferenceResult(final=final, categories=cats_np.copy(), per_layer=per,
                            elapsed_seconds=elapsed, edges_processed=inputs.total_inputs * edges,
@@ -1111,7 +1207,7 @@ def _one_layer(features: FeatureBatch, prepared: PreparedLayer, bias: np.ndarray
     s = int(ws.counts[1].item())
     alive = np.zeros(m, dtype=bool)
     alive[ws.a[1][:s].cpu().numpy()] = True
-    return out.cpu().numpy().T, alive
+    return d2h_numpy(out).T, alive
 
 
 def optimized_layer(features: FeatureBatch, prepared, bias: np.ndarray,
