@@ -814,8 +814,8 @@ def infer_device(net: DeviceNetwork, inputs: FeatureBatch, values: bool = True,
         raise ModelError("inputs do not match model width")
     edges = inputs.total_inputs * (edges_per_input if edges_per_input is not None
                                    else sum(getattr(net, "nnz", [])))
-    if not values and net.num_layers and m >= 4 * PIPELINE_MIN_FEATURES:
-        res = _infer_pipelined(net, inputs, edges)
+    if net.num_layers and m >= 4 * PIPELINE_MIN_FEATURES:
+        res = _infer_pipelined(net, inputs, edges, values)
         if res is not None:
             return res
     if net.num_layers == 0 or m == 0:
@@ -905,14 +905,19 @@ class _PipeBuffers:
         self.up = torch.cuda.Stream(device=device)
 
 
-def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
-    """values=False inference with the input upload overlapped: the batch is
+def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int,
+                     values: bool = False):
+    """Inference with the input upload overlapped: the batch is
     cut into two feature ranges (features never interact, so each runs the
     whole network on its own): a head (pipeline_head: sized so its compute
     covers the rest's upload) whose upload is the only one exposed, and the
     rest, copied host->device on a side stream while the head's layers run;
     one extra launch per layer is paid. One host synchronisation at the end
-    reads every chunk's counts.
+    reads every chunk's counts. With ``values`` the head's surviving values
+    are gathered (one host read of its count) once the rest's upload has been
+    issued and before the rest's layers reuse the feature buffers; categories
+    increase with the input position, so the head's sorted survivors precede
+    the rest's.
     Returns None when an arithmetic guard fired (the caller then takes the
     unchunked path, which reruns in the exact form)."""
     torch = _torch()
@@ -943,6 +948,21 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
     t0 = time.perf_counter()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(main)
+    vals_parts = []
+
+    def gather_values(c):
+        # chunk c's sorted survivors and their values (before the next chunk's
+        # input transpose and layers overwrite the feature buffers)
+        s_c = int(pb.counts[c][L].item())
+        o = L % 2
+        sc_cats, perm = torch.sort(pb.cat[c][o][:s_c])
+        out = torch.empty((s_c, n), dtype=torch.float32, device=ws.y[o].device)
+        if s_c:
+            _native.check(lib.spdnn_gather_out(
+                _dptr(ws.y[o]), n, ws.ld, _dptr(pb.a[c][o]), _dptr(perm), s_c, _dptr(out),
+                _stream_ptr(torch)), "spdnn_gather_out")
+        vals_parts.append(out)
+
     for c, (lo, hi) in enumerate(bounds):
         mc, xb = hi - lo, pb.x[c % 2]
         with torch.cuda.stream(up):
@@ -952,6 +972,8 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
             pb.cat[c][0][:mc].copy_(cats[lo:hi], non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(up)
+        if values and c > 0:
+            gather_values(c - 1)
         main.wait_event(ready)
         guard = ctypes.c_void_p(pb.guard.data_ptr() + 4 * c)
         _native.check(lib.spdnn_transpose_in(
@@ -975,6 +997,8 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
             _dptr(pb.a[c][0]), _dptr(pb.a[c][1]), _dptr(pb.cat[c][0]), _dptr(pb.cat[c][1]),
             _dptr(cnt), ctypes.byref(sc), ctypes.byref(opts), _stream_ptr(torch)),
             "spdnn_infer_layers")
+    if values:
+        gather_values(chunks - 1)
     ev1.record(main)
     host_counts = torch.cat([pb.counts.reshape(-1).to(torch.int64),
                              pb.guard.to(torch.int64)]).cpu().numpy()
@@ -985,7 +1009,13 @@ def _infer_pipelined(net: DeviceNetwork, inputs: FeatureBatch, edges: int):
     surv = counts[:, L]
     cat_parts = [pb.cat[c][L % 2][: int(surv[c])] for c in range(chunks)]
     cats_np = torch.sort(torch.cat(cat_parts))[0].cpu().numpy().astype(np.int64)
-    return InferenceResult(final=None, categories=cats_np, per_layer=_outcomes(counts.sum(0), net),
+    final = None
+    if values:
+        vals = vals_parts[0] if chunks == 1 else torch.cat(vals_parts)
+        final = FeatureBatch(neurons=n, data=d2h_numpy(vals).T, categories=cats_np,
+                             total_inputs=inputs.total_inputs)
+    return InferenceResult(final=final, categories=cats_np.copy() if values else cats_np,
+                           per_layer=_outcomes(counts.sum(0), net),
                            elapsed_seconds=elapsed, edges_processed=edges,
                            device_seconds=ev0.elapsed_time(ev1) / 1e3)
 

@@ -349,16 +349,28 @@ def test_chunked_device_network_infer_device(cuda_ok):
         [(o.active_before, o.active_after) for o in want.per_layer]
 
 
-def test_pipelined_upload_matches_single_pass(cuda_ok):
-    """values=False on a large host batch takes the chunked upload/compute
-    pipeline (engine._infer_pipelined): same categories and per-layer counts as
-    the one-pass run and the oracle's; a NaN input makes it fall back to the
-    guarded path with the same answer."""
+def test_pipelined_upload_matches_single_pass(cuda_ok, monkeypatch):
+    """A large host batch takes the chunked upload/compute pipeline
+    (engine._infer_pipelined), with or without values: same categories,
+    per-layer counts and (bit for bit) final values as the one-pass run, and
+    the oracle's categories; a NaN input makes it fall back to the guarded
+    path with the same answer."""
     model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
         neurons=1024, layers=40, connections_per_neuron=32, bias_value=-0.3, seed=3))
     inputs = ingest.generate_synthetic_inputs(1024, 5 * engine.PIPELINE_MIN_FEATURES + 77, 0.3,
                                               seed=5)
-    full = engine.infer(model, inputs, InferenceConfig())
+    with monkeypatch.context() as mp:
+        mp.setattr(engine, "PIPELINE_MIN_FEATURES", 1 << 40)  # one pass
+        full = engine.infer(model, inputs, InferenceConfig())
+    piped_v = engine.infer(model, inputs, InferenceConfig())
+    assert np.array_equal(piped_v.categories, full.categories)
+    assert np.array_equal(piped_v.final.categories, full.final.categories)
+    assert same_bits(piped_v.final.data, full.final.data)
+    # a pageable (numpy) batch goes through the staged host copies
+    pageable = make_feature_batch(1024, np.array(inputs.data, order="F"), inputs.categories,
+                                  total_inputs=inputs.total_inputs)
+    again = engine.infer(model, pageable, InferenceConfig())
+    assert same_bits(again.final.data, full.final.data)
     piped = engine.infer(model, inputs, InferenceConfig(), values=False)
     assert piped.final is None
     assert np.array_equal(piped.categories, full.categories)
