@@ -300,6 +300,10 @@ def host_tensor(a: np.ndarray):
 # ~2 GB/s into fresh memory (first-touch page faults inside the copy); here the
 # bytes go through two reused pinned chunks, the CPU side copied by a few
 # threads (page faults in parallel) while the DMA of the other chunk runs.
+# The chunks are per device and shared by every caller thread: a transfer
+# holds the device's staging lock from its first chunk until its last copy has
+# completed (concurrent infer calls, test_engine.py:264-287 of the reference,
+# take turns on the copy engine instead of overwriting each other's chunks).
 
 STAGE_CHUNK = 32 << 20
 _STAGE_THREADS = 8
@@ -313,7 +317,8 @@ def _stage_buffers(torch, dev):
         if st is None:
             bufs = [torch.empty(STAGE_CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
             from concurrent.futures import ThreadPoolExecutor
-            st = (bufs, [b.numpy() for b in bufs], ThreadPoolExecutor(_STAGE_THREADS))
+            st = (bufs, [b.numpy() for b in bufs], ThreadPoolExecutor(_STAGE_THREADS),
+                  threading.Lock())
             _stage[dev] = st
         return st
 
@@ -338,24 +343,25 @@ def d2h_numpy(src) -> np.ndarray:
     if nbytes < (4 << 20):
         out[...] = src.cpu().numpy()
         return out
-    bufs, views, pool = _stage_buffers(torch, src.device.index)
+    bufs, views, pool, lock = _stage_buffers(torch, src.device.index)
     s8 = src.reshape(-1).view(torch.uint8)
     o8 = out.reshape(-1).view(np.uint8)
     stream = torch.cuda.current_stream()
     events = [torch.cuda.Event(), torch.cuda.Event()]
     pending = None  # (buffer index, offset, length) copied to the GPU, not yet to `out`
-    for i, off in enumerate(range(0, nbytes, STAGE_CHUNK)):
-        b, ln = i % 2, min(STAGE_CHUNK, nbytes - off)
-        bufs[b][:ln].copy_(s8[off:off + ln], non_blocking=True)
-        events[b].record(stream)
-        if pending is not None:
-            pb_, poff, pln = pending
-            events[pb_].synchronize()
-            _par_copy(pool, o8[poff:poff + pln], views[pb_][:pln])
-        pending = (b, off, ln)
-    pb_, poff, pln = pending
-    events[pb_].synchronize()
-    _par_copy(pool, o8[poff:poff + pln], views[pb_][:pln])
+    with lock:
+        for i, off in enumerate(range(0, nbytes, STAGE_CHUNK)):
+            b, ln = i % 2, min(STAGE_CHUNK, nbytes - off)
+            bufs[b][:ln].copy_(s8[off:off + ln], non_blocking=True)
+            events[b].record(stream)
+            if pending is not None:
+                pb_, poff, pln = pending
+                events[pb_].synchronize()
+                _par_copy(pool, o8[poff:poff + pln], views[pb_][:pln])
+            pending = (b, off, ln)
+        pb_, poff, pln = pending
+        events[pb_].synchronize()
+        _par_copy(pool, o8[poff:poff + pln], views[pb_][:pln])
     return out
 
 
@@ -369,22 +375,23 @@ def h2d_into(dst, src: np.ndarray) -> None:
     if t.is_pinned() or src.nbytes < (4 << 20):
         dst.copy_(t.reshape(dst.shape), non_blocking=True)
         return
-    bufs, views, pool = _stage_buffers(torch, dst.device.index)
+    bufs, views, pool, lock = _stage_buffers(torch, dst.device.index)
     d8 = dst.reshape(-1).view(torch.uint8)
     s8 = src.reshape(-1).view(np.uint8)
     stream = torch.cuda.current_stream()
     events = [None, None]
-    for i, off in enumerate(range(0, src.nbytes, STAGE_CHUNK)):
-        b, ln = i % 2, min(STAGE_CHUNK, src.nbytes - off)
-        if events[b] is not None:
-            events[b].synchronize()  # the chunk that used this buffer has been copied
-        _par_copy(pool, views[b][:ln], s8[off:off + ln])
-        d8[off:off + ln].copy_(bufs[b][:ln], non_blocking=True)
-        events[b] = torch.cuda.Event()
-        events[b].record(stream)
-    for e in events:
-        if e is not None:
-            e.synchronize()
+    with lock:
+        for i, off in enumerate(range(0, src.nbytes, STAGE_CHUNK)):
+            b, ln = i % 2, min(STAGE_CHUNK, src.nbytes - off)
+            if events[b] is not None:
+                events[b].synchronize()  # the chunk that used this buffer has been copied
+            _par_copy(pool, views[b][:ln], s8[off:off + ln])
+            d8[off:off + ln].copy_(bufs[b][:ln], non_blocking=True)
+            events[b] = torch.cuda.Event()
+            events[b].record(stream)
+        for e in events:
+            if e is not None:
+                e.synchronize()
 
 
 def _dptr(t) -> ctypes.c_void_p:

@@ -389,6 +389,54 @@ def test_pipelined_upload_matches_single_pass(cuda_ok, monkeypatch):
     assert np.array_equal(a.categories, b.categories)
 
 
+def test_concurrent_staged_transfers_and_infer(cuda_ok):
+    """Pageable host buffers go through one pair of pinned chunks per device
+    (engine.h2d_into / d2h_numpy); concurrent callers (the reference's
+    concurrent-infer contract, pkg/tests/test_engine.py:264-287) must take
+    turns on them: every thread's bytes come back unchanged, and concurrent
+    infer calls on staged (pageable, multi-chunk) batches give the
+    single-threaded answers bit for bit."""
+    import threading
+    from concurrent.futures import ThreadPoolExecutor
+    import torch
+
+    def roundtrip(seed):
+        src = np.random.default_rng(seed).integers(0, 1 << 31, 3 * engine.STAGE_CHUNK // 4 + 12345,
+                                                  dtype=np.int32)
+        dst = torch.empty(src.shape, dtype=torch.int32, device="cuda")
+        for _ in range(3):
+            engine.h2d_into(dst, src)
+            back = engine.d2h_numpy(dst)
+            if not np.array_equal(back, src):
+                return False
+        return True
+
+    with ThreadPoolExecutor(4) as ex:
+        assert all(ex.map(roundtrip, range(8)))
+
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=1024, layers=12, connections_per_neuron=32, bias_value=-0.3, seed=21))
+    m = 2 * engine.STAGE_CHUNK // (4 * 1024) + 333  # > 2 staging chunks per batch
+    batches = []
+    for i in range(3):
+        b = ingest.generate_synthetic_inputs(1024, m, 0.3, seed=30 + i)
+        batches.append(make_feature_batch(1024, np.array(b.data, order="F"), b.categories,
+                                          total_inputs=b.total_inputs))
+    want = [engine.infer(model, b, InferenceConfig()) for b in batches]
+    barrier = threading.Barrier(3)
+
+    def run(i):
+        barrier.wait()
+        return i, engine.infer(model, batches[i], InferenceConfig())
+
+    with ThreadPoolExecutor(3) as ex:
+        for i, got in ex.map(run, range(3)):
+            assert np.array_equal(got.categories, want[i].categories)
+            assert same_bits(got.final.data, want[i].final.data)
+            assert [(o.active_before, o.active_after) for o in got.per_layer] == \
+                [(o.active_before, o.active_after) for o in want[i].per_layer]
+
+
 def test_two_features_per_lane_variant(cuda_ok, monkeypatch):
     """The 64-feature-item kernel variant (FPL = 2, 28 consumer warps) is an
     alternative launch configuration of the same layout: same bits."""
