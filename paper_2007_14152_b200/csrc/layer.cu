@@ -1327,8 +1327,9 @@ struct LaunchCache {
 };
 LaunchCache g_launch;
 
-int device_info(int &sms, size_t &optin) {
-  int dev;
+// (the caller's current device is returned in `dev`: g_dev may be switched to
+// another device by a concurrent caller as soon as the lock is released)
+int device_info(int &dev, int &sms, size_t &optin) {
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   std::lock_guard<std::mutex> lk(g_dev.mu);
   if (g_dev.device != dev) {
@@ -1352,9 +1353,9 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   if (!fn) return spdnn_fail(SPDNN_EINVAL, "layer: rows_per_group must be 1 or 3..7");
   if (MASK != (L.uniform != 0) || (MASK && L.record_words != 1))
     return spdnn_fail(SPDNN_EINVAL, "layer: record format does not match the layout");
-  int sms;
+  int dev, sms;
   size_t optin;
-  if (device_info(sms, optin)) return spdnn_fail(SPDNN_ECUDA, "layer: no CUDA device");
+  if (device_info(dev, sms, optin)) return spdnn_fail(SPDNN_ECUDA, "layer: no CUDA device");
   auto up128 = [](size_t x) { return (x + 127) / 128 * 128; };
   const size_t meta = up128((size_t)L.max_meta_per_block * 4);
   const size_t rec = up128((size_t)L.max_records_per_stage * L.record_words * 4 + 16);
@@ -1406,7 +1407,7 @@ int launch_layer(LayerArgs &A, bool fma, cudaStream_t stream, bool pdl) {
   int per_sm = 0;
   {
     std::lock_guard<std::mutex> lk(g_launch.mu);
-    LaunchCache::Entry &en = g_launch.map[std::make_pair(g_dev.device, fn)];
+    LaunchCache::Entry &en = g_launch.map[std::make_pair(dev, fn)];
     if (smem > en.smem_set) {
       cudaError_t e0 = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem);
