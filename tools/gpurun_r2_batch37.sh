@@ -1,4 +1,5 @@
 # consumer cohort offset: half of every SMSP's consumer warps start their first unit N ns late
+# (SPDNN_COHORT_NS lived in layer.cu for this run only; removed after it measured no change)
 mkdir -p gpurun_out
 out=gpurun_out/b37.txt; : > $out
 for rep in 1 2; do
