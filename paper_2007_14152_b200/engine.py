@@ -72,7 +72,7 @@ class InferenceResult:
 @dataclass(frozen=True)
 class PlanParams:
     """Kernel geometry knobs of the row-grouped union layout."""
-    rows_per_group: int = 0      # 0 = cost model picks 1, 3 or 7 per layer; 6 on request
+    rows_per_group: int = 0      # 0 = cost model: 1, 3 or 7 (6 for mask layers >= 8192 rows)
     footprint_cap: int = 176     # staged input neurons per block stage (x512 B smem)
     max_groups: int = 20         # row groups per block (one per consumer warp)
     record_cap: int = 800        # union records per block stage

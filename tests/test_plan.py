@@ -102,6 +102,28 @@ def test_sliding_window_layers_group_well():
         assert plan.num_fp / 4096 < 1.35
 
 
+def test_large_mask_layers_group_six_rows():
+    """Mask-record layers of >= 8192 rows take R = 6 (measured faster on the
+    16384- and 65536-neuron networks): ~K+5 union records per
+    group, bit-exact through the emulator; per-row weight records and smaller
+    layers keep the cost model's R = 7."""
+    rng = np.random.default_rng(23)
+    n = 8192
+    model = ingest.generate_synthetic_network(
+        ingest.GeneratorSpec(neurons=n, layers=2, connections_per_neuron=32, seed=4))
+    for layer in model.layers:
+        plan = _check(layer, PlanParams(), rng, m=3)
+        assert plan.rows_per_group == 6
+        assert plan.num_records / (n / 6) < 40.5  # 37 records, runs padded to 4
+    small = ingest.generate_synthetic_network(
+        ingest.GeneratorSpec(neurons=n - 1, layers=1, connections_per_neuron=32, seed=4))
+    assert build_plans(small.layers, PlanParams())[0].rows_per_group == 7
+    lay = model.layers[0]
+    vals = (rng.uniform(0.01, 0.2, lay.nnz) * rng.choice([-1, 1], lay.nnz)).astype(np.float32)
+    weighted = make_layer_csr(n, np.repeat(np.arange(n), 32), lay.col_idx, vals)
+    assert build_plans([weighted], PlanParams())[0].rows_per_group == 7
+
+
 def test_identical_rows_form_classes():
     """Windows shared by thousands of rows (offset/stride ratio with 2-adic
     valuation >= 10 in the generator; each column fans out to > 512 rows):
