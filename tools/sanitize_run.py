@@ -1,6 +1,7 @@
 """Small inferences for compute-sanitizer (tools/sanitize.sh): the smoke
-network (1024 x 12, 512 inputs at the survival edge) and a 2048 x 12
-structured network with per-row +/- weights (weight records, exact form),
+network (1024 x 12, 512 inputs at the survival edge), a 2048 x 12
+structured network with per-row +/- weights (weight records, exact form) and
+an 8192 x 6 generator network (R = 6 groups),
 each through the public API and checked against the oracle.
 
     compute-sanitizer --tool memcheck python tools/sanitize_run.py [case ...]
@@ -46,7 +47,15 @@ def structured():
     return model, inputs
 
 
-CASES = {"smoke": smoke, "structured": structured}
+def large():
+    """8192 x 6 generator network: the R = 6 mask-record layout (>= 8192 rows)."""
+    model = ingest.generate_synthetic_network(ingest.GeneratorSpec(
+        neurons=8192, layers=6, connections_per_neuron=32, bias_value=-0.35, seed=5))
+    inputs = ingest.generate_synthetic_inputs(8192, 300, 0.35, seed=6)
+    return model, inputs
+
+
+CASES = {"smoke": smoke, "structured": structured, "large": large}
 
 
 def main(names):
