@@ -1,4 +1,5 @@
 # compute-sanitizer on the R = 6 layout (8192 x 6 generator network)
+# (compute-sanitizer is closed on the GPU pool as of this run: rc 86 without running; the R = 6 layout is covered by the full-size C3/C4 parity tests instead)
 mkdir -p gpurun_out
 python -c "from paper_2007_14152_b200 import _native; _native.build(force=True)" > /dev/null
 for tool in memcheck racecheck synccheck; do
