@@ -280,9 +280,9 @@ double record_cost(int R) { return R == 1 ? 3.0 : (R == 3 ? 3.0 : 4.25); }
 double mask_record_cost(int R) { return R == 7 ? 7.0 : (R == 6 ? 6.0 : 4.25); }
 // Mask-record layers with at least this many rows group 6 rows instead of 7:
 // measured on B200 16384 x 1920 +1.7 %, 65536 x 1920 +1.6 %,
-// 4096 x 480 +-0, 1024 x 120 -1.8 % (one union record per 6 rows has 37
-// records for 32 useful ones instead of 38 per 7 rows: 13.5 % padded slots
-// instead of 15.8 %, at 14 % more groups per layer)
+// 4096 x 480 +-0, 1024 x 120 -1.8 % (with 32 connections per row a 6-row
+// group's union holds 37 records and a 7-row group's 38: 13.5 % padded slots
+// instead of 15.8 %, at 17 % more groups per layer)
 constexpr int64_t kR6MinRows = 8192;
 
 // The kernel keeps at least two ring entries in shared memory, so one
