@@ -1212,7 +1212,15 @@ __global__ void __launch_bounds__(Geo<FPL, MASK>::kThreads, 1)
   for (;; ) {
     const char *buf = smem + slot * A.buf_bytes;
     mbar_wait(full0 + 8 * slot, phase);  // (launch_layer: never a stale phase)
-    const Header h = *reinterpret_cast<const Header *>(buf);
+    // the whole header in two 16-byte loads issued together (the fields are
+    // otherwise loaded one by one behind the branches that test them)
+    Header h;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(h.item), "=r"(h.entry), "=r"(h.t), "=r"(h.b)
+                 : "r"((uint32_t)__cvta_generic_to_shared(buf)));
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(h.nst), "=r"(h.ng), "=r"(h.rec_cnt), "=r"(h.fp_cnt)
+                 : "r"((uint32_t)__cvta_generic_to_shared(buf) + 16));
     if (warp == 0 && k == 0) LTRACE(2, gtime());
     if (warp == 0) TRACE(k, 5);
     if (warp == C - 1) TRACE(k, 8);
